@@ -1,0 +1,149 @@
+/* moep_b200.h — C ABI of the B200-native pre-attention expert predictor.
+ *
+ * Drop-in boundary for the hot path of the reference `moepredict` package
+ * (arXiv 2511.10676). The reference has no FFI: its "operator API" is the
+ * Python function surface listed in pkg/src/moepredict/__init__.py:5-118.
+ * Each entry point below replaces the arithmetic behind one of those
+ * functions; the Python package `paper_2511_10676_b200` binds them with
+ * ctypes and keeps the reference's names, argument meaning and exceptions.
+ *
+ * Conventions (all entry points):
+ *   - plain device pointers + explicit sizes, no torch types;
+ *   - `stream` is a cudaStream_t passed as void*;
+ *   - no allocation, no host synchronisation; scratch comes from the caller;
+ *   - return 0 on success, a negative MOEP_E* code otherwise.
+ * Layouts: row-major, bf16 = IEEE bfloat16 bit patterns (uint16).
+ */
+#ifndef MOEP_B200_H
+#define MOEP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MOEP_OK = 0,
+  MOEP_ESHAPE = -1,       /* inconsistent or unsupported dimensions       -> ConfigurationError */
+  MOEP_EALIGN = -2,       /* pointer / stride alignment (TMA needs 16 B)  -> ConfigurationError */
+  MOEP_EUNSUPPORTED = -3, /* configuration outside this kernel's envelope -> ValueError        */
+  MOEP_ELAUNCH = -4,      /* CUDA launch / driver failure                 -> RuntimeError      */
+  MOEP_EARG = -5          /* bad argument value (m out of range, ...)     -> ValueError        */
+};
+
+#define MOEP_MAX_BOUNDS 4
+
+/* Counter block layout produced by the evaluation kernels (int64 after the
+ * final reduce; int32 per-CTA partials before it):
+ *   [0] n_rows  [1] top1  [2 .. 2+n_m) overprov[m]  [2+n_m .. 2+2n_m) recall[m]
+ *   [2+2n_m .. +E) per_expert_hits   [2+2n_m+E .. +E) per_expert_truth
+ * Replaces the integer core of metrics.evaluate_predictions (metrics.py:138-193). */
+static inline int32_t moep_n_counters(int32_t n_m, int32_t n_experts) {
+  return 2 + 2 * n_m + 2 * n_experts;
+}
+
+/* ------------------------------------------------------------------ K1 --
+ * Fused predictor over bf16 activations: GEMM1 (tcgen05, fp32 TMEM) -> bias +
+ * activation -> hi/lo bf16 split -> GEMM2 (tcgen05) -> +b2 -> per-token
+ * top-m selection, near-tie margin flag, optional fused evaluation counters.
+ * Replaces predictor.predict_logits / predict_topk_batch (predictor.py:330-351,
+ * _forward_internal eval branch :193-240) and core.top_k_batch (core.py:42-48).
+ * Tokens whose selection is not provably exact (margin < tau) are flagged and
+ * appended to flag_list; moep_predict_fp64 must then be run on them. */
+typedef struct {
+  int64_t n_tokens;
+  int32_t d, hidden, n_experts;
+  int32_t arch;               /* 1: BN(eval)+GELU-tanh, 2: SiLU */
+  const void* x;              /* [N, d] bf16 */
+  const void* w1;             /* [hidden, d] bf16 */
+  const float* b1;            /* [hidden] (arch2) */
+  const float* act_alpha;     /* [hidden] arch1: folded BN scale/sqrt(var+eps) */
+  const float* act_beta;      /* [hidden] arch1: folded shift - mean*alpha + b1*alpha */
+  const void* w2;             /* [E, hidden] bf16 */
+  const float* b2;            /* [E] */
+  int32_t m_sel;              /* ids per token written to `ids` (0: none; <= 15 or == E) */
+  int32_t n_bounds;           /* margin-check boundaries (positions), <= MOEP_MAX_BOUNDS */
+  int32_t bounds[MOEP_MAX_BOUNDS];
+  float tau_abs, tau_rel;     /* flag when gap < tau_abs + tau_rel*||h||*w2_norm */
+  float w2_norm;              /* max_e ||w2[e,:]||_2 */
+  int32_t* ids;               /* [N, m_sel] ascending, or NULL */
+  float* logits;              /* [N, E] fp32, or NULL */
+  uint8_t* flags;             /* [N], or NULL */
+  int32_t* flag_list;         /* [N] compacted flagged rows */
+  int32_t* flag_count;        /* [1] device counter (caller zeroes) */
+  const int32_t* truth;       /* [N, k] true expert ids, or NULL (no evaluation) */
+  int32_t k;
+  int32_t n_m;
+  int32_t m_list[MOEP_MAX_BOUNDS];
+  int32_t* partials;          /* [moep_num_sms(), n_counters] int32 */
+} moep_predict_args;
+
+int moep_predict_bf16(const moep_predict_args* a, void* stream);
+
+/* ------------------------------------------------------------------ K2 --
+ * fp64 predictor on CUDA cores, mirroring the reference's float64 op order
+ * per token (predictor.py:193-240, masked sigmoid :39-45). Runs on either all
+ * rows (rows == NULL) or the rows listed in rows[0 .. *row_count).
+ * Weights/activations may be bf16 or fp64 (dtype codes below). Writes fp64
+ * logits, top-m ids, and evaluation partials for the rows it handles. */
+enum { MOEP_BF16 = 1, MOEP_F64 = 2, MOEP_F32 = 3 };
+typedef struct {
+  int64_t n_tokens;
+  int32_t d, hidden, n_experts;
+  int32_t arch;
+  int32_t x_dtype, w_dtype;   /* MOEP_BF16 or MOEP_F64 */
+  const void* x;              /* [N, d] */
+  const void* w1;             /* [hidden, d] */
+  const double* b1;
+  const double* bn_scale, *bn_shift, *bn_mean, *bn_var;  /* arch1 */
+  double bn_eps;
+  const void* w2;             /* [E, hidden] */
+  const double* b2;
+  const int32_t* rows;        /* NULL = all rows */
+  const int32_t* row_count;   /* device scalar when rows != NULL */
+  int32_t m_sel;
+  int32_t* ids;               /* [N, m_sel] or NULL */
+  double* logits64;           /* [N, E] or NULL */
+  float* logits32;            /* [N, E] or NULL (patched copy of K1 output) */
+  const int32_t* truth; int32_t k; int32_t n_m; int32_t m_list[MOEP_MAX_BOUNDS];
+  int32_t* partials;          /* [moep_num_sms(), n_counters] */
+} moep_fp64_args;
+
+int moep_predict_fp64(const moep_fp64_args* a, void* stream);
+
+/* ------------------------------------------------------------------ K7 --
+ * Evaluation / selection from given logits (fp64 or fp32), exact compares.
+ * Replaces metrics.evaluate_predictions (metrics.py:138-193) and
+ * core.top_k_batch (core.py:42-48) / rank_order (:51-54). */
+int moep_eval_logits(const void* logits, int32_t dtype, int64_t n, int32_t n_experts,
+                     const int32_t* truth, int32_t k, int32_t n_m, const int32_t* m_list,
+                     int32_t* partials, void* stream);
+int moep_topk_logits(const void* logits, int32_t dtype, int64_t n, int32_t n_experts, int32_t m,
+                     int32_t* ids, void* stream);
+/* Full stable descending order per row (core.rank_order, core.py:51-54). */
+int moep_rank_order(const void* logits, int32_t dtype, int64_t n, int32_t n_experts, int32_t* order,
+                    void* stream);
+/* Deterministic sum of `n_blocks` int32 partial rows -> int64 counters. */
+int moep_counters_reduce(const int32_t* partials, int32_t n_blocks, int32_t n_counters,
+                         int64_t* out, void* stream);
+
+/* ------------------------------------------------------------------ K0 --
+ * Pre-attention input norm: fp64 statistics, output rounded fp64 -> bf16 RNE.
+ * kind: 0 none (cast), 1 rmsnorm(gamma, eps), 2 layernorm(gamma, beta, eps).
+ * x dtype: MOEP_BF16, MOEP_F32 or MOEP_F64. Also reports non-finite input
+ * through status[0] (ConfigurationError contract of predictor.py:188-189) and,
+ * for kind 0, counts rows holding values that are not bf16-representable in
+ * status[1] (those inputs take the fp64 path). status is int32[2], caller-zeroed. */
+int moep_input_norm(const void* x, int32_t x_dtype, int64_t n, int32_t d, int32_t kind,
+                    const double* gamma, const double* beta, double eps, void* xhat_bf16,
+                    int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------- misc -- */
+int moep_num_sms(void);
+const char* moep_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOEP_B200_H */

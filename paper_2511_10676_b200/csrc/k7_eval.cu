@@ -1,0 +1,314 @@
+// k7_eval.cu — K7: exact selection and evaluation counters from given logits,
+// the deterministic counter reduce, the input-norm kernel K0, and misc C ABI.
+//
+// moep_eval_logits restates metrics.evaluate_predictions (metrics.py:138-193):
+// the stable predicted rank of each true expert (core.rank_order, core.py:51-54)
+// is an exact count of keys ordered before it, computed one warp per token with
+// ballots; per-CTA partial counters are written without global atomics and
+// summed in a fixed order by moep_counters_reduce.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "common.cuh"
+
+namespace moep {
+namespace k7 {
+
+constexpr int NT = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(NT)
+eval_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict__ truth, int k,
+            int n_m, const int* __restrict__ m_list_dev, int* partials, int n_counters) {
+  extern __shared__ int sh[];  // [8 warps][2E] hist
+  __shared__ int scal[8][2 + 2 * MOEP_MAX_BOUNDS];
+  __shared__ int mls[MOEP_MAX_BOUNDS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* hist = sh + warp * 2 * E;
+  for (int i = lane; i < 2 * E; i += 32) hist[i] = 0;
+  if (threadIdx.x < MOEP_MAX_BOUNDS) mls[threadIdx.x] = threadIdx.x < n_m ? m_list_dev[threadIdx.x] : 0;
+  __syncthreads();
+  int cnt[2 + 2 * MOEP_MAX_BOUNDS];
+#pragma unroll
+  for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) cnt[i] = 0;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  for (int64_t row = gw; row < n; row += nwarps) {
+    const T* zr = z + row * E;
+    int tr[16];
+    int any0 = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      tr[j] = 0;
+      if (j < k) {
+        const int t = truth[row * k + j];
+        const T zt = zr[t];
+        int r = 0;
+        for (int e0 = 0; e0 < E; e0 += 32) {
+          const int e = e0 + lane;
+          const bool before = e < E && key_gt(zr[e < E ? e : 0], e, zt, t);
+          r += __popc(__ballot_sync(0xffffffffu, before));
+        }
+        tr[j] = r;
+        any0 |= r == 0;
+        if (lane == 0) {
+          hist[E + t] += 1;
+          if (r < k) hist[t] += 1;
+        }
+      }
+    }
+    cnt[0] += 1;
+    cnt[1] += any0;
+#pragma unroll
+    for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
+      if (mi < n_m) {
+        int inside = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) inside += (j < k && tr[j] < mls[mi]) ? 1 : 0;
+        cnt[2 + mi] += inside == k;
+        cnt[2 + MOEP_MAX_BOUNDS + mi] += inside;
+      }
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) scal[warp][i] = cnt[i];
+  }
+  __syncthreads();
+  int* out = partials + static_cast<int64_t>(blockIdx.x) * n_counters;
+  for (int t = threadIdx.x; t < n_counters; t += NT) {
+    int v = 0;
+    if (t < 2 + 2 * n_m) {
+      const int src = t < 2 ? t : (t < 2 + n_m ? t : 2 + MOEP_MAX_BOUNDS + (t - 2 - n_m));
+      for (int w = 0; w < NT / 32; ++w) v += scal[w][src];
+    } else {
+      const int e = t - 2 - 2 * n_m;
+      for (int w = 0; w < NT / 32; ++w) v += sh[w * 2 * E + e];
+    }
+    out[t] = v;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT)
+topk_kernel(const T* __restrict__ z, int64_t n, int E, int m, int* __restrict__ ids) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  for (int64_t row = gw; row < n; row += nwarps) {
+    const T* zr = z + row * E;
+    int written = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      bool sel = false;
+      if (e < E) {
+        const T ze = zr[e];
+        int r = 0;
+        for (int j = 0; j < E && r < m; ++j) r += key_gt(zr[j], j, ze, e) ? 1 : 0;
+        sel = r < m;
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+      if (sel) ids[row * m + written + __popc(bal & ((1u << lane) - 1u))] = e;
+      written += __popc(bal);
+    }
+  }
+}
+
+// Full stable descending order: order[rank(e)] = e, rank by exact key counts.
+template <typename T>
+__global__ void __launch_bounds__(NT)
+order_kernel(const T* __restrict__ z, int64_t n, int E, int* __restrict__ order) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  for (int64_t row = gw; row < n; row += nwarps) {
+    const T* zr = z + row * E;
+    for (int e = lane; e < E; e += 32) {
+      const T ze = zr[e];
+      int r = 0;
+      for (int j = 0; j < E; ++j) r += key_gt(zr[j], j, ze, e) ? 1 : 0;
+      order[row * E + r] = e;
+    }
+  }
+}
+
+__global__ void reduce_kernel(const int* __restrict__ partials, int n_blocks, int n_counters,
+                              long long* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_counters; c += gridDim.x * blockDim.x) {
+    long long s = 0;
+    for (int b = 0; b < n_blocks; ++b) s += partials[static_cast<int64_t>(b) * n_counters + c];
+    out[c] = s;
+  }
+}
+
+// ------------------------------------------------------------- K0: input norm
+template <int XT>
+__device__ __forceinline__ double ldx(const void* p, int64_t i) {
+  if (XT == MOEP_BF16) return static_cast<double>(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]));
+  if (XT == MOEP_F32) return static_cast<double>(reinterpret_cast<const float*>(p)[i]);
+  return reinterpret_cast<const double*>(p)[i];
+}
+
+__device__ double block_sum(double v, double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < NT / 32; ++w) t += red[w];
+  return t;
+}
+
+template <int XT>
+__global__ void __launch_bounds__(NT)
+norm_kernel(const void* x, int64_t n, int d, int kind, const double* gamma, const double* beta,
+            double eps, __nv_bfloat16* out, int* status) {
+  __shared__ double red[NT / 32];
+  for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
+    int bad = 0, inexact = 0;
+    double mu = 0.0, scale = 1.0;
+    if (kind != 0) {
+      double s = 0.0, s2 = 0.0;
+      for (int i = threadIdx.x; i < d; i += NT) {
+        const double v = ldx<XT>(x, row * d + i);
+        bad |= !isfinite(v);
+        s += v;
+        s2 += v * v;
+      }
+      const double sum = block_sum(s, red);
+      if (kind == 1) {
+        const double ms = block_sum(s2, red) / d;
+        scale = sqrt(ms + eps);
+      } else {
+        mu = sum / d;
+        double sv = 0.0;
+        for (int i = threadIdx.x; i < d; i += NT) {
+          const double c = ldx<XT>(x, row * d + i) - mu;
+          sv += c * c;
+        }
+        scale = sqrt(block_sum(sv, red) / d + eps);
+      }
+    }
+    for (int i = threadIdx.x; i < d; i += NT) {
+      const double v = ldx<XT>(x, row * d + i);
+      double y;
+      if (kind == 0) {
+        y = v;
+        bad |= !isfinite(v);
+      } else if (kind == 1) {
+        y = v / scale;
+        if (gamma) y = y * gamma[i];
+      } else {
+        y = (v - mu) / scale;
+        if (gamma) y = y * gamma[i];
+        if (beta) y = y + beta[i];
+      }
+      const __nv_bfloat16 b = f64_to_bf16_rne(y);
+      if (kind == 0) inexact |= static_cast<double>(__bfloat162float(b)) != y;
+      out[row * d + i] = b;
+    }
+    if (bad) atomicAdd(status, 1);
+    if (inexact) atomicAdd(status + 1, 1);
+  }
+}
+
+}  // namespace k7
+}  // namespace moep
+
+extern "C" {
+
+int moep_num_sms(void) {
+  static int cached[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+const char* moep_version(void) { return "moep_b200 0.1 sm_100a"; }
+
+int moep_eval_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, const int32_t* truth,
+                     int32_t k, int32_t n_m, const int32_t* m_list, int32_t* partials, void* stream) {
+  using namespace moep::k7;
+  if (n <= 0 || E <= 0) return MOEP_ESHAPE;
+  if (k < 1 || k > 16 || k > E || n_m < 1 || n_m > MOEP_MAX_BOUNDS) return MOEP_EARG;
+  const int ncnt = moep_n_counters(n_m, E);
+  const size_t smem = sizeof(int) * 2 * E * (NT / 32);
+  if (smem > 200 * 1024) return MOEP_EUNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = moep_num_sms();
+  if (dtype == MOEP_F64) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(eval_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    eval_kernel<double><<<grid, NT, smem, st>>>(static_cast<const double*>(logits), n, E, truth, k, n_m, m_list, partials, ncnt);
+  } else if (dtype == MOEP_F32) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(eval_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    eval_kernel<float><<<grid, NT, smem, st>>>(static_cast<const float*>(logits), n, E, truth, k, n_m, m_list, partials, ncnt);
+  } else {
+    return MOEP_EARG;
+  }
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+int moep_topk_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, int32_t m, int32_t* ids,
+                     void* stream) {
+  using namespace moep::k7;
+  if (n <= 0 || E <= 0) return MOEP_ESHAPE;
+  if (m < 1 || m > E) return MOEP_EARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = moep_num_sms() * 4;
+  if (dtype == MOEP_F64)
+    topk_kernel<double><<<grid, NT, 0, st>>>(static_cast<const double*>(logits), n, E, m, ids);
+  else if (dtype == MOEP_F32)
+    topk_kernel<float><<<grid, NT, 0, st>>>(static_cast<const float*>(logits), n, E, m, ids);
+  else
+    return MOEP_EARG;
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+int moep_rank_order(const void* logits, int32_t dtype, int64_t n, int32_t E, int32_t* order,
+                     void* stream) {
+  using namespace moep::k7;
+  if (n <= 0 || E <= 0) return MOEP_ESHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = moep_num_sms() * 4;
+  if (dtype == MOEP_F64)
+    order_kernel<double><<<grid, NT, 0, st>>>(static_cast<const double*>(logits), n, E, order);
+  else if (dtype == MOEP_F32)
+    order_kernel<float><<<grid, NT, 0, st>>>(static_cast<const float*>(logits), n, E, order);
+  else
+    return MOEP_EARG;
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+int moep_counters_reduce(const int32_t* partials, int32_t n_blocks, int32_t n_counters, int64_t* out,
+                         void* stream) {
+  if (n_blocks <= 0 || n_counters <= 0) return MOEP_ESHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  moep::k7::reduce_kernel<<<(n_counters + 255) / 256, 256, 0, st>>>(
+      partials, n_blocks, n_counters, reinterpret_cast<long long*>(out));
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+int moep_input_norm(const void* x, int32_t x_dtype, int64_t n, int32_t d, int32_t kind,
+                    const double* gamma, const double* beta, double eps, void* xhat_bf16,
+                    int32_t* status, void* stream) {
+  using namespace moep::k7;
+  if (n <= 0 || d <= 0) return MOEP_ESHAPE;
+  if (kind < 0 || kind > 2 || !status) return MOEP_EARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = static_cast<int>(n < 65536 ? n : 65536);
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(xhat_bf16);
+  if (x_dtype == MOEP_BF16) norm_kernel<MOEP_BF16><<<grid, NT, 0, st>>>(x, n, d, kind, gamma, beta, eps, out, status);
+  else if (x_dtype == MOEP_F32) norm_kernel<MOEP_F32><<<grid, NT, 0, st>>>(x, n, d, kind, gamma, beta, eps, out, status);
+  else if (x_dtype == MOEP_F64) norm_kernel<MOEP_F64><<<grid, NT, 0, st>>>(x, n, d, kind, gamma, beta, eps, out, status);
+  else return MOEP_EARG;
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+}  // extern "C"

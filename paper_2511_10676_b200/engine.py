@@ -1,0 +1,367 @@
+"""Device engine: a PredictorModel resident in HBM plus the kernel pipeline
+K0 (input cast / norm) -> K1 (fused tcgen05 predictor) -> K2 (fp64 near-tie
+fix-up) -> counter reduce, all enqueued on the caller's CUDA stream.
+
+Precision contract: the tensor-core path (K1) is used when
+the activations and both weight matrices are exactly bf16-representable. K1
+computes logits to ~1e-6 and flags every token whose selection gap is below
+    delta = tau_abs + tau_rel * ||h||_2 * max_e ||w2_e||_2 ;
+flagged tokens are recomputed in fp64 by K2 so predicted expert ids match the
+float64 reference bit for bit. Inputs that are not bf16-representable go to K2
+for every token (exact, fp64 CUDA cores).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import MOEP_BF16, MOEP_F64, check, lib, ptr
+from .exceptions import ConfigurationError
+
+K1_MAX_SEL = 15       # K1 keeps 16 sorted positions per token
+K1_MAX_EXPERTS = 128  # TMEM budget of the single-CTA kernel
+TAU_ABS = 1e-7
+TAU_REL = 2e-6
+
+
+def _require_cuda(device) -> torch.device:
+    dev = torch.device(device)
+    if dev.type != "cuda" or not torch.cuda.is_available():
+        raise RuntimeError("the B200 predictor needs a CUDA device (there is no CPU path)")
+    return dev
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _bf16_exact(t64: torch.Tensor) -> bool:
+    return bool(torch.equal(t64.to(torch.bfloat16).to(torch.float64), t64))
+
+
+@dataclass
+class EvalCounters:
+    """Integer result of the fused evaluation (layout of moep_n_counters)."""
+
+    n: int
+    k: int
+    n_experts: int
+    m_values: list
+    top1: int
+    overprov: dict
+    recall: dict
+    per_expert_hits: np.ndarray
+    per_expert_truth: np.ndarray
+    flagged: int = 0
+
+    @classmethod
+    def from_array(cls, c: np.ndarray, k, e, m_values, flagged=0):
+        n_m = len(m_values)
+        return cls(
+            n=int(c[0]), k=k, n_experts=e, m_values=list(m_values), top1=int(c[1]),
+            overprov={m: int(c[2 + i]) for i, m in enumerate(m_values)},
+            recall={m: int(c[2 + n_m + i]) for i, m in enumerate(m_values)},
+            per_expert_hits=c[2 + 2 * n_m: 2 + 2 * n_m + e].astype(np.int64),
+            per_expert_truth=c[2 + 2 * n_m + e: 2 + 2 * n_m + 2 * e].astype(np.int64),
+            flagged=flagged)
+
+    def __add__(self, o: "EvalCounters") -> "EvalCounters":
+        return EvalCounters(
+            self.n + o.n, self.k, self.n_experts, self.m_values, self.top1 + o.top1,
+            {m: self.overprov[m] + o.overprov[m] for m in self.m_values},
+            {m: self.recall[m] + o.recall[m] for m in self.m_values},
+            self.per_expert_hits + o.per_expert_hits, self.per_expert_truth + o.per_expert_truth,
+            self.flagged + o.flagged)
+
+
+class DevicePredictor:
+    """HBM-resident predictor weights in the layouts the kernels read.
+
+    bf16 w1 [h, d] / w2 [E, h] (K-major, TMA-swizzled on load), fp32 biases or
+    folded BN affine for the K1 epilogue, fp64 biases/BN state for K2; fp64
+    weight copies only when the model's weights are not bf16-representable.
+    """
+
+    def __init__(self, model, device="cuda", tau_abs=TAU_ABS, tau_rel=TAU_REL):
+        self.device = _require_cuda(device)
+        lib()
+        self.arch = model.arch
+        self.arch_code = 1 if model.arch == "arch1" else 2
+        self.d, self.hidden, self.E = model.d, model.hidden, model.n_experts
+        self.tau_abs, self.tau_rel = float(tau_abs), float(tau_rel)
+        dev = self.device
+        f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+        w1 = f64(model.w1)
+        w2 = f64(model.w2)
+        self.weights_bf16_exact = _bf16_exact(w1) and _bf16_exact(w2)
+        self.w1_bf16 = w1.to(torch.bfloat16).contiguous()
+        self.w2_bf16 = w2.to(torch.bfloat16).contiguous()
+        self.w1_f64 = None if self.weights_bf16_exact else w1
+        self.w2_f64 = None if self.weights_bf16_exact else w2
+        self.b1_f64, self.b2_f64 = f64(model.b1), f64(model.b2)
+        self.b1_f32, self.b2_f32 = self.b1_f64.float(), self.b2_f64.float()
+        self.bn_eps = float(getattr(model, "bn_eps", 1e-5))
+        if self.arch == "arch1":
+            self.bn = [f64(getattr(model, n)) for n in ("bn_scale", "bn_shift", "bn_mean", "bn_var")]
+            scale, shift, mean, var = self.bn
+            alpha = scale * (1.0 / torch.sqrt(var + self.bn_eps))
+            self.alpha = alpha.float().contiguous()
+            self.beta = (alpha * (self.b1_f64 - mean) + shift).float().contiguous()
+        else:
+            self.bn = [None] * 4
+            self.alpha = self.beta = None
+        self.w2_norm = float(torch.linalg.vector_norm(w2, dim=1).max()) if self.E else 0.0
+        self.n_sms = lib().moep_num_sms()
+
+    @classmethod
+    def for_model(cls, model, device="cuda", **kw) -> "DevicePredictor":
+        return cls(model, device, **kw)
+
+    # ---------------------------------------------------------------- inputs
+    def prepare(self, x: torch.Tensor, check_finite: bool = True):
+        """K0 cast: x (any float dtype, on device) -> bf16 copy, plus whether
+        every value was bf16-representable. Raises ConfigurationError on
+        non-finite input (predictor.py:188-189)."""
+        x = x.to(self.device)
+        if x.dim() != 2 or x.shape[1] != self.d:
+            raise ConfigurationError(f"input shape {tuple(x.shape)} incompatible with d={self.d}")
+        code = {torch.bfloat16: MOEP_BF16, torch.float64: MOEP_F64, torch.float32: _lib.MOEP_F32}.get(x.dtype)
+        if code is None:
+            x = x.to(torch.float64)
+            code = MOEP_F64
+        x = x.contiguous()
+        n = x.shape[0]
+        if x.dtype == torch.bfloat16:
+            xb = x
+            status = torch.zeros(2, dtype=torch.int32, device=self.device)
+            if check_finite:
+                bad = int((~torch.isfinite(x)).any())
+                status[0] = bad
+        else:
+            xb = torch.empty((n, self.d), dtype=torch.bfloat16, device=self.device)
+            status = torch.zeros(2, dtype=torch.int32, device=self.device)
+            check(lib().moep_input_norm(ptr(x), code, n, self.d, 0, None, None, 0.0, ptr(xb),
+                                        ptr(status), _stream(self.device)), "moep_input_norm")
+        st = status.cpu().numpy()
+        if st[0]:
+            raise ConfigurationError("input must be finite")
+        return x, xb, int(st[1]) == 0
+
+    def normalize(self, x: torch.Tensor, kind: str, gamma=None, beta=None, eps=None) -> torch.Tensor:
+        """K0 fused input norm (rmsnorm / layernorm, fp64 stats) -> bf16 x_hat."""
+        kinds = {"none": 0, "rmsnorm": 1, "layernorm": 2}
+        if kind not in kinds:
+            raise ConfigurationError(f"unknown norm kind {kind!r}")
+        eps = (1e-6 if kind == "rmsnorm" else 1e-5) if eps is None else eps
+        x = x.to(self.device).contiguous()
+        code = {torch.bfloat16: MOEP_BF16, torch.float64: MOEP_F64, torch.float32: _lib.MOEP_F32}[x.dtype]
+        out = torch.empty(x.shape, dtype=torch.bfloat16, device=self.device)
+        status = torch.zeros(2, dtype=torch.int32, device=self.device)
+        g = None if gamma is None else torch.as_tensor(gamma, dtype=torch.float64, device=self.device)
+        b = None if beta is None else torch.as_tensor(beta, dtype=torch.float64, device=self.device)
+        check(lib().moep_input_norm(ptr(x), code, x.shape[0], x.shape[1], kinds[kind], ptr(g), ptr(b),
+                                    float(eps), ptr(out), ptr(status), _stream(self.device)),
+              "moep_input_norm")
+        return out
+
+    # --------------------------------------------------------------- kernels
+    def _fp64_args(self, x, x_code, rows=None, row_count=None, m_sel=0, ids=None, logits64=None,
+                   logits32=None, truth=None, k=0, m_values=(), partials=None):
+        a = _lib.Fp64Args()
+        a.n_tokens, a.d, a.hidden, a.n_experts, a.arch = x.shape[0], self.d, self.hidden, self.E, self.arch_code
+        a.x_dtype = x_code
+        exact_w = self.weights_bf16_exact
+        a.w_dtype = MOEP_BF16 if exact_w else MOEP_F64
+        a.x = ptr(x)
+        a.w1 = ptr(self.w1_bf16 if exact_w else self.w1_f64)
+        a.w2 = ptr(self.w2_bf16 if exact_w else self.w2_f64)
+        a.b1, a.b2 = ptr(self.b1_f64), ptr(self.b2_f64)
+        a.bn_scale, a.bn_shift, a.bn_mean, a.bn_var = (ptr(t) for t in self.bn)
+        a.bn_eps = self.bn_eps
+        a.rows, a.row_count = ptr(rows), ptr(row_count)
+        a.m_sel, a.ids, a.logits64, a.logits32 = m_sel, ptr(ids), ptr(logits64), ptr(logits32)
+        a.truth, a.k, a.n_m = ptr(truth), k, len(m_values)
+        for i, m in enumerate(m_values):
+            a.m_list[i] = m
+        a.partials = ptr(partials)
+        return a
+
+    def _k1(self, xb, m_sel=0, bounds=(), ids=None, logits=None, truth=None, k=0, m_values=(),
+            partials=None):
+        n = xb.shape[0]
+        flags = torch.empty(n, dtype=torch.uint8, device=self.device)
+        flag_list = torch.empty(n, dtype=torch.int32, device=self.device)
+        flag_count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        a = _lib.PredictArgs()
+        a.n_tokens, a.d, a.hidden, a.n_experts, a.arch = n, self.d, self.hidden, self.E, self.arch_code
+        a.x, a.w1, a.w2 = ptr(xb), ptr(self.w1_bf16), ptr(self.w2_bf16)
+        a.b1, a.b2 = ptr(self.b1_f32), ptr(self.b2_f32)
+        a.act_alpha, a.act_beta = ptr(self.alpha), ptr(self.beta)
+        a.m_sel = m_sel
+        a.n_bounds = len(bounds)
+        for i, b in enumerate(bounds):
+            a.bounds[i] = b
+        a.tau_abs, a.tau_rel, a.w2_norm = self.tau_abs, self.tau_rel, self.w2_norm
+        a.ids, a.logits, a.flags = ptr(ids), ptr(logits), ptr(flags)
+        a.flag_list, a.flag_count = ptr(flag_list), ptr(flag_count)
+        a.truth, a.k, a.n_m = ptr(truth), k, len(m_values)
+        for i, m in enumerate(m_values):
+            a.m_list[i] = m
+        a.partials = ptr(partials)
+        check(lib().moep_predict_bf16(a, _stream(self.device)), "moep_predict_bf16")
+        return flags, flag_list, flag_count
+
+    def k1_usable(self, exact_x: bool, positions=()) -> bool:
+        return (exact_x and self.weights_bf16_exact and self.E <= K1_MAX_EXPERTS
+                and self.d % 8 == 0 and self.hidden % 8 == 0
+                and all(p <= K1_MAX_SEL or p >= self.E for p in positions))
+
+    # ------------------------------------------------------------------ API
+    def logits(self, x: torch.Tensor, return_flags=False):
+        """fp64 logits [N, E] (predict_logits)."""
+        x, xb, exact = self.prepare(x)
+        n = x.shape[0]
+        out64 = torch.empty((n, self.E), dtype=torch.float64, device=self.device)
+        if self.k1_usable(exact):
+            lg = torch.empty((n, self.E), dtype=torch.float32, device=self.device)
+            flags, flist, fcount = self._k1(xb, logits=lg)
+            out64.copy_(lg)
+            a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, logits64=out64)
+            check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
+        else:
+            code = MOEP_F64 if x.dtype == torch.float64 else MOEP_BF16
+            xs = x if code == MOEP_F64 or x.dtype == torch.bfloat16 else x.to(torch.float64)
+            code = MOEP_BF16 if xs.dtype == torch.bfloat16 else MOEP_F64
+            a = self._fp64_args(xs, code, logits64=out64)
+            check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
+            flags = None
+        return (out64, flags) if return_flags else out64
+
+    def topk(self, x: torch.Tensor, m: int, return_flags=False):
+        """Ascending top-m expert ids [N, m] (predict_topk_batch)."""
+        if not 1 <= m <= self.E:
+            raise ValueError(f"m={m} out of range for {self.E} experts")
+        x, xb, exact = self.prepare(x)
+        n = x.shape[0]
+        ids = torch.empty((n, m), dtype=torch.int32, device=self.device)
+        flags = None
+        if self.k1_usable(exact, (m,)):
+            bounds = (m,) if m < self.E else ()
+            flags, flist, fcount = self._k1(xb, m_sel=m, bounds=bounds, ids=ids)
+            a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, m_sel=m, ids=ids)
+        else:
+            xs = x if x.dtype in (torch.float64, torch.bfloat16) else x.to(torch.float64)
+            code = MOEP_BF16 if xs.dtype == torch.bfloat16 else MOEP_F64
+            a = self._fp64_args(xs, code, m_sel=m, ids=ids)
+        check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
+        return (ids, flags) if return_flags else ids
+
+    def evaluate(self, x: torch.Tensor, truth: torch.Tensor, k: int, m_values, ids_m: int = 0,
+                 prepared=None) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+        """Fused predict + evaluation counters on device.
+
+        Returns (counters int64 [n_counters], flag_count int32 [1], ids or None)
+        without synchronising; see EvalCounters.from_array for the layout.
+        """
+        m_values = sorted(set(int(m) for m in m_values))
+        if k not in m_values:
+            m_values.insert(0, k)
+        if prepared is None:
+            x, xb, exact = self.prepare(x)
+        else:
+            x, xb, exact = prepared
+        n = x.shape[0]
+        truth = truth.to(device=self.device, dtype=torch.int32).contiguous()
+        ncnt = 2 + 2 * len(m_values) + 2 * self.E
+        partials = torch.empty((2 * self.n_sms, ncnt), dtype=torch.int32, device=self.device)
+        counters = torch.empty(ncnt, dtype=torch.int64, device=self.device)
+        ids = torch.empty((n, ids_m), dtype=torch.int32, device=self.device) if ids_m else None
+        positions = sorted({1, k, *m_values, *( [ids_m] if ids_m else [])})
+        bounds = tuple(p for p in positions if p < self.E)
+        if len(m_values) <= _lib.MAX_BOUNDS and len(bounds) <= _lib.MAX_BOUNDS and self.k1_usable(exact, bounds) \
+                and k <= 16:
+            flags, flist, fcount = self._k1(xb, m_sel=ids_m, bounds=bounds, ids=ids, truth=truth, k=k,
+                                            m_values=m_values, partials=partials[: self.n_sms])
+            a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, m_sel=ids_m, ids=ids,
+                                truth=truth, k=k, m_values=m_values, partials=partials[self.n_sms:])
+            check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
+            check(lib().moep_counters_reduce(ptr(partials), 2 * self.n_sms, ncnt, ptr(counters),
+                                             _stream(self.device)), "moep_counters_reduce")
+            return counters, fcount, ids
+        # general path: exact fp64 logits for every token, then K7 from logits
+        z = self.logits_fp64_all(x)
+        counters = eval_logits_device(z, truth, k, self.E, m_values)
+        if ids_m:
+            ids = topk_logits_device(z, ids_m)
+        return counters, torch.zeros(1, dtype=torch.int32, device=self.device), ids
+
+    def logits_fp64_all(self, x):
+        xs = x if x.dtype in (torch.float64, torch.bfloat16) else x.to(torch.float64)
+        code = MOEP_BF16 if xs.dtype == torch.bfloat16 else MOEP_F64
+        out64 = torch.empty((x.shape[0], self.E), dtype=torch.float64, device=self.device)
+        a = self._fp64_args(xs, code, logits64=out64)
+        check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
+        return out64
+
+
+# ----------------------------------------------------------- logits kernels
+def eval_logits_device(z: torch.Tensor, truth: torch.Tensor, k: int, e: int, m_values) -> torch.Tensor:
+    """K7 counters from given logits; m_values of any length (chunked by 4)."""
+    dev = z.device
+    z = z.contiguous()
+    code = MOEP_F64 if z.dtype == torch.float64 else _lib.MOEP_F32
+    if z.dtype not in (torch.float64, torch.float32):
+        z = z.to(torch.float64)
+        code = MOEP_F64
+    truth = truth.to(device=dev, dtype=torch.int32).contiguous()
+    n = z.shape[0]
+    m_values = list(m_values)
+    n_sms = lib().moep_num_sms()
+    scal = []
+    hist = None
+    top1 = n_rows = None
+    for s in range(0, len(m_values), _lib.MAX_BOUNDS):
+        ms = m_values[s: s + _lib.MAX_BOUNDS]
+        ncnt = 2 + 2 * len(ms) + 2 * e
+        part = torch.empty((n_sms, ncnt), dtype=torch.int32, device=dev)
+        mdev = torch.tensor(ms, dtype=torch.int32, device=dev)
+        check(lib().moep_eval_logits(ptr(z), code, n, e, ptr(truth), k, len(ms), ptr(mdev), ptr(part),
+                                     _stream(dev)), "moep_eval_logits")
+        c = torch.empty(ncnt, dtype=torch.int64, device=dev)
+        check(lib().moep_counters_reduce(ptr(part), n_sms, ncnt, ptr(c), _stream(dev)), "moep_counters_reduce")
+        nm = len(ms)
+        n_rows, top1 = c[0:1], c[1:2]
+        scal.append((c[2: 2 + nm], c[2 + nm: 2 + 2 * nm]))
+        hist = c[2 + 2 * nm:]
+    ov = torch.cat([a for a, _ in scal])
+    rc = torch.cat([b for _, b in scal])
+    return torch.cat([n_rows, top1, ov, rc, hist])
+
+
+def topk_logits_device(z: torch.Tensor, m: int) -> torch.Tensor:
+    dev = z.device
+    z = z.contiguous()
+    if z.dtype not in (torch.float64, torch.float32):
+        z = z.to(torch.float64)
+    code = MOEP_F64 if z.dtype == torch.float64 else _lib.MOEP_F32
+    n, e = z.shape
+    ids = torch.empty((n, m), dtype=torch.int32, device=dev)
+    check(lib().moep_topk_logits(ptr(z), code, n, e, m, ptr(ids), _stream(dev)), "moep_topk_logits")
+    return ids
+
+
+def rank_order_device(z: torch.Tensor) -> torch.Tensor:
+    """Exact stable descending order per row (K7 moep_rank_order)."""
+    dev = z.device
+    z = z.contiguous()
+    if z.dtype not in (torch.float64, torch.float32):
+        z = z.to(torch.float64)
+    code = MOEP_F64 if z.dtype == torch.float64 else _lib.MOEP_F32
+    n, e = z.shape
+    order = torch.empty((n, e), dtype=torch.int32, device=dev)
+    check(lib().moep_rank_order(ptr(z), code, n, e, ptr(order), _stream(dev)), "moep_rank_order")
+    return order

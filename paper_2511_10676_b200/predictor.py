@@ -1,0 +1,210 @@
+"""Two-layer expert predictors — the reference API over the B200 kernels.
+
+Reference: pkg/src/moepredict/predictor.py. Names, signatures, shapes, the
+1-D convenience form and the exception contract are kept:
+
+    arch1: linear -> batch-norm -> GELU(tanh) -> dropout -> linear
+    arch2: linear -> SiLU -> linear
+
+`PredictorModel` stays a host object holding float64 parameters (so MOEPM1
+checkpoints round-trip bit-exactly, predictor.py:354-412); every arithmetic
+call uploads it into a `DevicePredictor` (engine.py) and runs the sm_100a
+kernels. numpy in -> numpy float64 out; CUDA tensors in -> CUDA tensors out.
+For a resident model across many calls use `DevicePredictor` directly.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .core import ExpertSelection
+from .engine import DevicePredictor
+from .exceptions import BadMagicError, ConfigurationError, UsageError, VersionError
+
+CHECKPOINT_MAGIC = b"MOEPM1"
+CHECKPOINT_VERSION = 1
+_CKPT_HEADER = struct.Struct("<5I")
+ARCHS = ("arch1", "arch2")
+
+
+@dataclass
+class PredictorModel:
+    """Parameters and normalisation state of one per-layer predictor
+    (reference predictor.py:75-136)."""
+
+    arch: str
+    w1: np.ndarray
+    b1: np.ndarray
+    w2: np.ndarray
+    b2: np.ndarray
+    bn_scale: np.ndarray | None = None
+    bn_shift: np.ndarray | None = None
+    bn_mean: np.ndarray | None = None
+    bn_var: np.ndarray | None = None
+    dropout_rate: float = 0.1
+    bn_momentum: float = 0.1
+    bn_eps: float = 1e-5
+    mode: str = "eval"
+    dropout_seed: int = 0
+    _dropout_step: int = field(default=0, repr=False)
+    _cache: dict | None = field(default=None, repr=False)
+
+    def __post_init__(self):
+        if self.arch not in ARCHS:
+            raise ConfigurationError(f"unknown arch {self.arch!r}")
+        has_bn = all(v is not None for v in (self.bn_scale, self.bn_shift, self.bn_mean, self.bn_var))
+        if self.arch == "arch1" and not has_bn:
+            raise ConfigurationError("arch1 requires batch-norm state")
+        if self.arch == "arch2" and has_bn:
+            raise ConfigurationError("arch2 carries no batch-norm state")
+        if self.bn_var is not None and np.any(np.asarray(self.bn_var) < 0):
+            raise ConfigurationError("running variance must be >= 0")
+
+    @property
+    def d(self) -> int:
+        return self.w1.shape[1]
+
+    @property
+    def hidden(self) -> int:
+        return self.w1.shape[0]
+
+    @property
+    def n_experts(self) -> int:
+        return self.w2.shape[0]
+
+    def train(self) -> "PredictorModel":
+        self.mode = "train"
+        return self
+
+    def eval(self) -> "PredictorModel":
+        self.mode = "eval"
+        self._cache = None
+        return self
+
+    def param_dict(self) -> dict:
+        params = {"w1": self.w1, "b1": self.b1, "w2": self.w2, "b2": self.b2}
+        if self.arch == "arch1":
+            params["bn_scale"] = self.bn_scale
+            params["bn_shift"] = self.bn_shift
+        return params
+
+    def to_device(self, device="cuda", **kw) -> DevicePredictor:
+        return DevicePredictor(self, device, **kw)
+
+
+def init_model(arch: str, d: int, hidden: int, n_experts: int, seed: int = 0,
+               dropout_rate: float = 0.1) -> PredictorModel:
+    """Kaiming-uniform fan-in init from the Philox(seed << 64) stream, so the
+    parameters are bit-identical to the reference's (predictor.py:139-173)."""
+    if arch not in ARCHS:
+        raise ConfigurationError(f"unknown arch {arch!r}")
+    rng = np.random.Generator(np.random.Philox(key=(int(seed) << 64)))
+    w1 = rng.uniform(-np.sqrt(1.0 / d), np.sqrt(1.0 / d), size=(hidden, d))
+    w2 = rng.uniform(-np.sqrt(1.0 / hidden), np.sqrt(1.0 / hidden), size=(n_experts, hidden))
+    b1, b2 = np.zeros(hidden), np.zeros(n_experts)
+    if arch == "arch1":
+        return PredictorModel(arch, w1, b1, w2, b2, bn_scale=np.ones(hidden), bn_shift=np.zeros(hidden),
+                              bn_mean=np.zeros(hidden), bn_var=np.ones(hidden),
+                              dropout_rate=dropout_rate, dropout_seed=seed)
+    return PredictorModel(arch, w1, b1, w2, b2, dropout_rate=0.0, dropout_seed=seed)
+
+
+def n_params(model: PredictorModel) -> int:
+    return int(sum(np.asarray(p).size for p in model.param_dict().values()))
+
+
+def _as_batch(model: PredictorModel, x):
+    """Shape contract of _check_input (predictor.py:180-190); finiteness is
+    checked on the device by K0 and raised as ConfigurationError."""
+    if isinstance(x, torch.Tensor):
+        single = x.dim() == 1
+        batch = x[None, :] if single else x
+        if batch.dim() != 2 or batch.shape[1] != model.d:
+            raise ConfigurationError(f"input shape {tuple(x.shape)} incompatible with d={model.d}")
+        return batch, single, True
+    x = np.asarray(x, dtype=np.float64)
+    single = x.ndim == 1
+    batch = x[None, :] if single else x
+    if batch.ndim != 2 or batch.shape[1] != model.d:
+        raise ConfigurationError(f"input shape {x.shape} incompatible with d={model.d}")
+    return torch.from_numpy(np.ascontiguousarray(batch)), single, False
+
+
+def predict_logits(model: PredictorModel, x):
+    """Eval-mode logits regardless of the mode flag (predictor.py:330-334)."""
+    batch, single, is_t = _as_batch(model, x)
+    z = DevicePredictor(model).logits(batch.to("cuda"))
+    if not is_t:
+        z = z.cpu().numpy()
+    return z[0] if single else z
+
+
+def predict_topk_batch(model: PredictorModel, x, m: int):
+    """Row-wise ascending top-m expert ids, shape (n, m) (predictor.py:347-351)."""
+    if not 1 <= m <= model.n_experts:
+        raise ValueError(f"m={m} out of range for {model.n_experts} experts")
+    batch, single, is_t = _as_batch(model, x)
+    ids = DevicePredictor(model).topk(batch.to("cuda"), m).to(torch.int64)
+    return ids if is_t else ids.cpu().numpy()
+
+
+def predict_topk(model: PredictorModel, x, m: int) -> ExpertSelection:
+    """Top-m selection for one activation vector (predictor.py:337-344)."""
+    if model.mode != "eval":
+        raise UsageError("predict_topk requires the model in eval mode")
+    if not 1 <= m <= model.n_experts:
+        raise ValueError(f"m={m} out of range for {model.n_experts} experts")
+    x = np.asarray(x, dtype=np.float64).reshape(-1)
+    dev = DevicePredictor(model)
+    batch = torch.from_numpy(x[None, :]).to("cuda")
+    logits = dev.logits(batch)[0].cpu().numpy()
+    ids = dev.topk(batch, m)[0].cpu().numpy()
+    return ExpertSelection(indices=ids.astype(np.int64), raw_scores=logits)
+
+
+def save_model(model: PredictorModel, path) -> None:
+    """MOEPM1 checkpoint, float64 parameters in fixed order (predictor.py:354-369)."""
+    arrays = [model.w1, model.b1, model.w2, model.b2]
+    if model.arch == "arch1":
+        arrays += [model.bn_scale, model.bn_shift, model.bn_mean, model.bn_var]
+    with open(path, "wb") as f:
+        f.write(CHECKPOINT_MAGIC)
+        f.write(_CKPT_HEADER.pack(CHECKPOINT_VERSION, 1 if model.arch == "arch1" else 2,
+                                  model.d, model.hidden, model.n_experts))
+        f.write(struct.pack("<d", float(model.dropout_rate)))
+        for arr in arrays:
+            f.write(np.ascontiguousarray(arr, dtype="<f8").tobytes())
+
+
+def load_model(path) -> PredictorModel:
+    """Read a MOEPM1 checkpoint; the model loads in eval mode (predictor.py:372-412)."""
+    with open(path, "rb") as f:
+        blob = f.read()
+    if blob[: len(CHECKPOINT_MAGIC)] != CHECKPOINT_MAGIC:
+        raise BadMagicError("not a predictor checkpoint")
+    off = len(CHECKPOINT_MAGIC)
+    version, arch_tag, d, hidden, e = _CKPT_HEADER.unpack_from(blob, off)
+    off += _CKPT_HEADER.size
+    if version != CHECKPOINT_VERSION:
+        raise VersionError(f"unsupported checkpoint version {version}")
+    if arch_tag not in (1, 2):
+        raise ConfigurationError(f"unknown arch tag {arch_tag}")
+    (dropout_rate,) = struct.unpack_from("<d", blob, off)
+    off += 8
+
+    def take(shape):
+        nonlocal off
+        count = int(np.prod(shape))
+        arr = np.frombuffer(blob, dtype="<f8", count=count, offset=off)
+        off += count * 8
+        return arr.astype(np.float64).reshape(shape)
+
+    w1, b1, w2, b2 = take((hidden, d)), take((hidden,)), take((e, hidden)), take((e,))
+    if arch_tag == 1:
+        return PredictorModel("arch1", w1, b1, w2, b2, bn_scale=take((hidden,)), bn_shift=take((hidden,)),
+                              bn_mean=take((hidden,)), bn_var=take((hidden,)), dropout_rate=dropout_rate)
+    return PredictorModel("arch2", w1, b1, w2, b2, dropout_rate=dropout_rate)
