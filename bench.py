@@ -1,0 +1,418 @@
+"""Benchmark: DeepSeek-V2-Lite-shaped pre-attention predictor inference + top-6
+accuracy evaluation over all MoE layers (BASELINE.json configs[1]).
+
+One step = every one of the 26 MoE layers' predictors (d=2048, h=2048, E=64,
+k=6, arch2, random Kaiming init rounded to bf16) run over 1,048,576 synthetic
+tokens per GPU, with the fused evaluation counters (m in {6, 10, 64}) and the
+fp64 near-tie fix-up that makes the ids bit-exact. Activations (4 GiB per
+layer, > L2) stay resident in HBM; `e2e` streams them from pinned host memory
+through the same public API instead.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+For N > 1 run under torchrun: tokens are sharded (weak scaling), the only
+collective is one int64 all-reduce of the evaluation counters per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D, H, E, K_ACT = 2048, 2048, 64, 6
+N_LAYERS = 26                      # DeepSeek-V2-Lite MoE layers (27 layers, first dense)
+TOKENS = 1 << 20                   # per GPU per layer
+M_LIST = [6, 10, 64]
+METRIC = "predictor tokens/s/GPU + top-k ID match; expert prefetch GB/s vs host link"
+FLOP_PER_TOKEN = 2 * (D * H + H * E)  # algorithmic, per token per layer
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p["bf16_tflops_sustained"]), float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ setup
+def make_layers(dev, n_layers, tokens, seed_base):
+    """Random-init predictors (reference init_model, bf16-rounded), synthetic
+    bf16 activations, and teacher-gate ground truth per layer."""
+    import torch
+    import paper_2511_10676_b200 as pb
+    layers = []
+    g = torch.Generator(device=dev)
+    for layer in range(n_layers):
+        model = pb.init_model("arch2", D, H, E, seed=layer)
+        model.w1 = _round_bf16_np(model.w1)
+        model.w2 = _round_bf16_np(model.w2)
+        dp = pb.DevicePredictor(model, dev)
+        g.manual_seed(seed_base + layer)
+        x = torch.randn((tokens, D), device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
+        gate = torch.randn((E, D), device=dev, generator=g, dtype=torch.float32) / np.sqrt(D)
+        xf = x.float()
+        xn = (xf - xf.mean(1, keepdim=True)) / torch.sqrt(xf.var(1, unbiased=False, keepdim=True) + 1e-5)
+        truth = torch.topk(xn @ gate.T, K_ACT, dim=1).indices.sort(dim=1).values.to(torch.int32)
+        del xf, xn
+        layers.append((model, dp, x, truth))
+    return layers
+
+
+def _round_bf16_np(a):
+    a = np.asarray(a, dtype=np.float64)
+    m, e = np.frexp(a)
+    return np.ldexp(np.rint(m * 256.0), e - 8)
+
+
+def step(layers, k1_events=None):
+    """One pass over every layer: fused predict + eval (K1), fp64 fix-up (K2), reduce."""
+    outs = []
+    for li, (_, dp, x, truth) in enumerate(layers):
+        prepared = (x, x, True)
+        if k1_events is not None:
+            k1_events[li][0].record()
+        cnt, fcount, _ = dp.evaluate(x, truth, K_ACT, M_LIST, prepared=prepared)
+        if k1_events is not None:
+            k1_events[li][1].record()
+        outs.append((cnt, fcount))
+    return outs
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=N_LAYERS)
+    ap.add_argument("--tokens", type=int, default=TOKENS)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    layers = make_layers(dev, args.layers, args.tokens, seed_base=1000 * rank)
+    n_tok_rank = args.tokens * args.layers
+
+    def all_reduce_counters(outs):
+        flat = torch.cat([c for c, _ in outs] + [f.to(torch.int64) for _, f in outs])
+        if world > 1:
+            dist.all_reduce(flat)
+        return flat
+
+    for _ in range(args.warmup):
+        all_reduce_counters(step(layers))
+    torch.cuda.synchronize()
+
+    # ---- timed region: device events around K steps, barrier + sync on both sides
+    k1_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.layers)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        start.record()
+        for s in range(args.steps):
+            flat = all_reduce_counters(step(layers, k1_ev[s]))
+        stop.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = start.elapsed_time(stop)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = world * n_tok_rank * args.steps / (ms_total / 1e3)
+
+    # per-launch time of the evaluate pipeline (K1 dominant) inside the timed region
+    per_layer_ms = [a.elapsed_time(b) for row in k1_ev for (a, b) in row]
+    pipe_ms = statistics.mean(per_layer_ms)
+
+    # counters of the last step (for the accuracy line and the flagged fraction)
+    import paper_2511_10676_b200 as pb
+    ncnt = 2 + 2 * 3 + 2 * E
+    flat_np = flat.cpu().numpy()
+    flagged = int(flat_np[args.layers * ncnt:].sum())
+    c0 = pb.EvalCounters.from_array(flat_np[:ncnt], K_ACT, E, M_LIST)
+
+    # K1 alone (same stream, events) for the roofline: time one layer's K1 launch
+    k1_ms = time_k1(layers[0][1], layers[0][2], layers[0][3], reps=5)
+    burst, sustained, hbm, src = peaks()
+    achieved_tflops = FLOP_PER_TOKEN * args.tokens / (k1_ms / 1e3) / 1e12
+
+    id_match = None
+    cpu = None
+    e2e = None
+    if rank == 0:
+        id_match = check_ids(layers[0], n_check=2048)
+        if not args.no_cpu:
+            cpu = cpu_baseline(layers[0][0], layers[0][2], layers[0][3], n_sample=32768)
+    if not args.no_e2e:
+        e2e = e2e_arm(layers, args, world, dev)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (N(0,1) activations rounded to bf16; random Kaiming-init predictors rounded "
+                    "to bf16; teacher-gate top-6 ground truth)",
+            "config": {"workload": "DeepSeek-V2-Lite all MoE layers: predictor inference + top-6 accuracy "
+                                   "eval (BASELINE configs[1])",
+                       "layers": args.layers, "tokens_per_gpu_per_layer": args.tokens, "d": D, "hidden": H,
+                       "experts": E, "k": K_ACT, "m_list": M_LIST, "arch": "arch2",
+                       "token_unit": "one token through one layer's predictor",
+                       "l2": "inputs larger than L2 (4 GiB of activations per layer)",
+                       "parallelism": f"token-sharded dp{world}"},
+            "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": sustained, "unit": "TFLOP/s",
+                         "frac": achieved_tflops / sustained, "peak_kind": f"{src} sustained bf16",
+                         "frac_of_burst": achieved_tflops / burst, "kernel": "moep k1 predict_kernel",
+                         "flop_per_token": FLOP_PER_TOKEN, "tokens_per_launch": args.tokens,
+                         "k1_ms_per_launch": k1_ms, "pipeline_ms_per_layer": pipe_ms, "traffic": None},
+            "gpu_launches": args.steps * args.layers * 3,
+            "clocks": clk.summary(),
+            "flagged_fraction": flagged / (args.layers * args.tokens * world),
+            "id_match": id_match,
+            "accuracy_layer0": {"exact_match": c0.overprov[K_ACT] / c0.n, "top1": c0.top1 / c0.n,
+                                "overprov10": c0.overprov[10] / c0.n},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def time_k1(dp, x, truth, reps=5):
+    """Average duration of the K1 launch alone (CUDA events on its stream)."""
+    import torch
+    n = x.shape[0]
+    ncnt = 2 + 2 * 3 + 2 * E
+    part = torch.empty((dp.n_sms, ncnt), dtype=torch.int32, device=x.device)
+    args = dict(m_sel=0, bounds=(1, 6, 10), truth=truth, k=K_ACT, m_values=M_LIST, partials=part)
+    dp._k1(x, **args)
+    torch.cuda.synchronize()
+    s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        dp._k1(x, **args)
+    t.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(t) / reps
+
+
+def check_ids(layer, n_check=2048):
+    """Bench-time parity: top-6 ids of the first n_check tokens vs the fp64 oracle."""
+    import torch
+    from oracle import oracle as O
+    model, dp, x, _ = layer
+    xs = x[:n_check]
+    ids = dp.topk(xs, K_ACT).cpu().numpy()
+    p = {"arch": "arch2", "w1": model.w1, "b1": model.b1, "w2": model.w2, "b2": model.b2}
+    ref = O.predict_topk_batch(p, xs.float().cpu().numpy().astype(np.float64), K_ACT)
+    return {"tokens_checked": n_check, "mismatching_tokens": int((ids != ref).any(axis=1).sum()),
+            "checker": "oracle/oracle.py fp64 restatement (pinned to reference goldens)"}
+
+
+def cpu_baseline(model, x, truth, n_sample=32768):
+    """The oracle port (numpy fp64, all host threads) on a bounded sample."""
+    from oracle import oracle as O
+    xs = x[:n_sample].float().cpu().numpy().astype(np.float64)
+    tr = truth[:n_sample].cpu().numpy().astype(np.int64)
+    p = {"arch": "arch2", "w1": model.w1, "b1": model.b1, "w2": model.w2, "b2": model.b2}
+    t0 = time.perf_counter()
+    z = O.predict_logits(p, xs)
+    O.top_k_batch(z, K_ACT)
+    O.evaluate_predictions(z, tr, E, M_LIST)
+    dt = time.perf_counter() - t0
+    return {"value": n_sample / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{n_sample} tokens of layer 0: predict_logits + top_k_batch(6) + evaluate_predictions "
+                      f"(oracle/oracle.py numpy fp64, OpenBLAS all threads), {dt:.2f} s"}
+
+
+def e2e_arm(layers, args, world, dev):
+    """Same metric through the public API with HOST activations: per layer, H2D of
+    the pinned activations + truth, fused predict/eval/fix-up, D2H of the counters.
+    Copies run on a side stream, double-buffered against compute."""
+    import torch
+    import torch.distributed as dist
+    tokens = args.tokens
+    host_x = [layers[i][2].cpu().pin_memory() for i in range(min(2, len(layers)))]
+    host_t = [layers[i][3].cpu().pin_memory() for i in range(min(2, len(layers)))]
+    dbuf = [torch.empty_like(layers[0][2]) for _ in range(2)]
+    tbuf = [torch.empty_like(layers[0][3]) for _ in range(2)]
+    copy = torch.cuda.Stream(dev)
+    comp = torch.cuda.current_stream(dev)
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    h_cnt = torch.empty((args.layers, 2 + 2 * 3 + 2 * E), dtype=torch.int64).pin_memory()
+    bytes_in = (host_x[0].numel() * 2 + host_t[0].numel() * 4) * args.layers
+    bytes_out = h_cnt.numel() * 8
+
+    def one_step():
+        for li in range(args.layers):
+            b = li % 2
+            with torch.cuda.stream(copy):
+                copy.wait_event(free[b])
+                dbuf[b].copy_(host_x[li % len(host_x)], non_blocking=True)
+                tbuf[b].copy_(host_t[li % len(host_t)], non_blocking=True)
+                ready[b].record(copy)
+            comp.wait_event(ready[b])
+            dp = layers[li][1]
+            cnt, _, _ = dp.evaluate(dbuf[b], tbuf[b], K_ACT, M_LIST, prepared=(dbuf[b], dbuf[b], True))
+            free[b].record(comp)
+            h_cnt[li].copy_(cnt, non_blocking=True)
+        if world > 1:
+            flat = h_cnt.to(dev)
+            dist.all_reduce(flat)
+    for b in range(2):
+        free[b].record(comp)
+    one_step()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    s.record()
+    for _ in range(steps):
+        one_step()
+    t.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(t)
+    tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    return {"value": world * tokens * args.layers * steps / (ms / 1e3), "unit": "tokens/s",
+            "h2d_bytes_per_step": bytes_in, "d2h_bytes_per_step": bytes_out, "steps": steps,
+            "api": "DevicePredictor.evaluate on device buffers filled from pinned host memory"}
+
+
+# ------------------------------------------------------------- reference arm
+def reference_arm(args, rank, world):
+    """The reference's CPU implementation of the path (the oracle port:
+    oracle/oracle.py restates moepredict's float64 numpy code) on the host cores,
+    on a bounded sample of the same workload per step. Rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    rng = np.random.default_rng(0)
+    n = 8192
+    p = O.init_params("arch2", D, H, E, seed=0)
+    p["w1"], p["w2"] = O.round_bf16(p["w1"]), O.round_bf16(p["w2"])
+    x = O.round_bf16(rng.standard_normal((n, D)))
+    gate = rng.standard_normal((E, D)) / np.sqrt(D)
+    truth = O.top_k_batch(O.layer_norm(x) @ gate.T, K_ACT)
+
+    def one():
+        z = O.predict_logits(p, x)
+        O.top_k_batch(z, K_ACT)
+        O.evaluate_predictions(z, truth, E, M_LIST)
+    for _ in range(max(1, min(args.warmup, 1))):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = time.perf_counter() - t0
+    value = n * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "DeepSeek-V2-Lite all MoE layers: predictor inference + top-6 accuracy eval "
+                               "(BASELINE configs[1]); each step is a bounded sample of one layer",
+                   "tokens_per_step": n, "d": D, "hidden": H, "experts": E, "k": K_ACT, "m_list": M_LIST},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{n} tokens x {args.steps} steps: predict_logits + top_k_batch + "
+                                   "evaluate_predictions, numpy fp64 / OpenBLAS all threads"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,7 @@ typedef struct {
   int32_t n_m;
   int32_t m_list[MOEP_MAX_BOUNDS];
   int32_t* partials;          /* [moep_num_sms(), n_counters] int32 */
+  float* a_out;               /* [N, hidden] fp32 pre-activation W1.x + b1 (training), or NULL */
 } moep_predict_args;
 
 int moep_predict_bf16(const moep_predict_args* a, void* stream);
@@ -98,7 +99,8 @@ typedef struct {
   const double* b1;
   const double* bn_scale, *bn_shift, *bn_mean, *bn_var;  /* arch1 */
   double bn_eps;
-  const void* w2;             /* [E, hidden] */
+  const void* w2;             /* [E, hidden] (informational; K2 reads w2t) */
+  const void* w2t;            /* [hidden, E] transposed W2, same dtype as w2 */
   const double* b2;
   const int32_t* rows;        /* NULL = all rows */
   const int32_t* row_count;   /* device scalar when rows != NULL */
@@ -108,6 +110,7 @@ typedef struct {
   float* logits32;            /* [N, E] or NULL (patched copy of K1 output) */
   const int32_t* truth; int32_t k; int32_t n_m; int32_t m_list[MOEP_MAX_BOUNDS];
   int32_t* partials;          /* [moep_num_sms(), n_counters] */
+  double* a_out;              /* [N, hidden] fp64 pre-activation (training, exact mode), or NULL */
 } moep_fp64_args;
 
 int moep_predict_fp64(const moep_fp64_args* a, void* stream);
@@ -138,6 +141,73 @@ int moep_counters_reduce(const int32_t* partials, int32_t n_blocks, int32_t n_co
 int moep_input_norm(const void* x, int32_t x_dtype, int64_t n, int32_t d, int32_t kind,
                     const double* gamma, const double* beta, double eps, void* xhat_bf16,
                     int32_t* status, void* stream);
+
+/* ------------------------------------------------------------ training --
+ * Every training entry point takes a dtype (MOEP_F64 or MOEP_F32) for its
+ * floating-point buffers: MOEP_F64 is the exact-parity mode (reference
+ * arithmetic in float64), MOEP_F32 the throughput mode (fp32 master weights,
+ * bf16 tensor-core forward).
+ *
+ * K3: BatchLabels.from_scores (losses.py:64-74): 1-based stable ranks, top-k
+ * mask, and per-token strict-pair counts among the true top-min(10,E). */
+int moep_labels(const void* scores, int32_t dtype, int64_t n, int32_t n_experts, int32_t k,
+                int32_t* rank_of, uint8_t* topk_mask, int32_t* pair_count, void* stream);
+
+/* K4: loss_and_grad (losses.py:243-273). family: 0 mse, 1 wbce, 2 focal,
+ * 3 ranking. Writes the per-element gradient (without the batch-global hinge
+ * normaliser) to dz / dz_hinge and 3 fp64 partials per CTA {loss, hinge,
+ * n_pairs}; moep_loss_finalize sums them in a fixed order (after an optional
+ * cross-rank all-reduce of the partial sums) and completes dz and the loss
+ * (out_loss[0] = loss, out_loss[1] = n_pairs).
+ * n_global = tokens over all data-parallel ranks (the N of N*E, losses.py:129). */
+typedef struct {
+  int32_t family;
+  double top_weight, mid_weight, rest_weight, ranking_lambda, margin, focal_gamma, focal_alpha;
+  int32_t normalize_ranking;
+  int64_t n, n_global;
+  int32_t n_experts;
+  int32_t dtype;              /* of logits / scores / dz / dz_hinge */
+  const void* logits;         /* [n, E] */
+  const void* scores;         /* [n, E] true affinity scores */
+  const int32_t* rank_of;     /* [n, E] from moep_labels */
+  const uint8_t* topk_mask;   /* [n, E] */
+  void* dz;                   /* [n, E] out */
+  void* dz_hinge;             /* [n, E] out (ranking) */
+  double* partials;           /* [n_blocks, 3] out */
+  int32_t n_blocks;
+} moep_loss_args;
+int moep_loss(const moep_loss_args* a, void* stream);
+int moep_loss_finalize(const double* partials, int32_t n_blocks, int64_t n, int32_t n_experts,
+                       int32_t family, double ranking_lambda, int32_t normalize, int32_t dtype,
+                       void* dz, const void* dz_hinge, double* out_loss, void* stream);
+
+/* K5: arch2 backward around the activation (predictor.py:261-297):
+ * dA = (dZ . W2) * silu'(a); dW2 = dZ^T . silu(a); db1 = sum dA; db2 = sum dZ.
+ * scratch: n_slices * (E*H + H + E) elements. dW1 = dA^T . X is a plain GEMM. */
+int moep_act_backward(const void* a, const void* dz, const void* w2, int32_t dtype, int64_t n,
+                      int32_t hidden, int32_t n_experts, int32_t n_slices, void* da, void* dw2,
+                      void* db1, void* db2, void* scratch, void* stream);
+
+/* K6: optimizer step on a flat master buffer (trainer.py:103-122).
+ * kind: 0 sgd, 1 momentum, 2 adam (bias-corrected with step t, 1-based).
+ * The first n_shadow parameters are also written as bf16 (the forward copy)
+ * when shadow_bf16 != NULL; *nonfinite counts CTAs that produced a non-finite
+ * parameter (the NaN guard of trainer.py:125-128). */
+typedef struct {
+  int32_t kind;
+  int32_t dtype;
+  int64_t n;
+  void* params;
+  const void* grads;
+  void* m;
+  void* v;
+  double lr, beta1, beta2, eps, momentum;
+  int64_t t;
+  void* shadow_bf16;
+  int64_t n_shadow;
+  int32_t* nonfinite;
+} moep_optim_args;
+int moep_optim_step(const moep_optim_args* a, void* stream);
 
 /* ---------------------------------------------------------------- misc -- */
 int moep_num_sms(void);

@@ -393,3 +393,47 @@ def teacher_scores(x, gate_w):
     """Router ground truth for synthetic activations: softmax(W_g . layer_norm(x))
     (synthgen.py:185-188 with post_norm=True; core.py:117-127)."""
     return softmax(layer_norm(x) @ np.asarray(gate_w, dtype=np.float64).T, axis=-1)
+
+
+# ------------------------------------------------------------ train loop
+def train_arch2(acts, scores, topk, k, *, hidden=32, batch_size=64, epochs=1, lr=1e-3, optimizer="adam",
+                seed=0, eval_fraction=0.1, loss=None, overprov_m=None, max_steps=None):
+    """Restatement of trainer.train for arch2 (trainer.py:131-204): Philox
+    shuffle/split, labels from the fp64 cast of the fp32 scores, minibatch
+    forward / loss_and_grad / backward / optimizer, held-out eval per epoch.
+    Returns (params, [(train_loss, exact, top1, overprov)], steps)."""
+    loss = loss or {"family": "wbce"}
+    n = acts.shape[0]
+    d, e = acts.shape[1], scores.shape[1]
+    m_over = overprov_m if overprov_m else min(e, k + 4)
+    rng = np.random.Generator(np.random.Philox(key=((int(seed) & 0xFFFFFFFFFFFFFFFF) << 64) + (1 << 61) + 7))
+    perm = rng.permutation(n)
+    n_eval = max(1, int(round(n * eval_fraction)))
+    tr_idx, ev_idx = perm[: n - n_eval], perm[n - n_eval:]
+    x_tr = acts[tr_idx].astype(np.float64)
+    lab = batch_labels(scores[tr_idx].astype(np.float64), k)
+    x_ev, tk_ev = acts[ev_idx].astype(np.float64), topk[ev_idx]
+    p = init_params("arch2", d, hidden, e, seed=seed)
+    state, t, steps, rows = {}, 0, 0, []
+    for _ in range(epochs):
+        order = rng.permutation(x_tr.shape[0])
+        loss_sum = 0.0
+        for start in range(0, x_tr.shape[0], batch_size):
+            b = order[start: start + batch_size]
+            lb = {kk: v[b] for kk, v in lab.items()}
+            z, cache = forward_eval(p, x_tr[b])  # arch2 train forward == eval forward
+            lv, dz = loss_and_grad(loss, z, lb)
+            g = backward_eval(p, cache, dz)
+            g = {kk: g[kk] for kk in ("w1", "b1", "w2", "b2")}
+            t += 1
+            if optimizer == "adam":
+                adam_step(p, g, state, t, lr=lr)
+            else:
+                sgd_step(p, g, state, lr, momentum=0.9 if optimizer == "momentum" else None)
+            loss_sum += lv * len(b)
+            steps += 1
+            if max_steps and steps >= max_steps:
+                return p, rows, steps
+        res = evaluate_predictions(predict_logits(p, x_ev), tk_ev, e, [m_over])
+        rows.append((loss_sum / x_tr.shape[0], res["exact_match"], res["top1"], res["overprov"][m_over]))
+    return p, rows, steps

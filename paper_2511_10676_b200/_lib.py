@@ -2,7 +2,8 @@
 
 The product path has no fallback: if the library is missing or no CUDA device
 is present, every compute entry point raises. Struct layouts below mirror the
-header field for field.
+header field for field (tests/test_capi.py checks sizes and offsets against a
+C compiler).
 """
 
 from __future__ import annotations
@@ -19,13 +20,6 @@ MOEP_OK, MOEP_ESHAPE, MOEP_EALIGN, MOEP_EUNSUPPORTED, MOEP_ELAUNCH, MOEP_EARG = 
 MOEP_BF16, MOEP_F64, MOEP_F32 = 1, 2, 3
 MAX_BOUNDS = 4
 
-EXPORTED = (
-    "moep_predict_bf16", "moep_predict_fp64", "moep_eval_logits", "moep_topk_logits",
-    "moep_counters_reduce", "moep_rank_order", "moep_input_norm", "moep_num_sms", "moep_version",
-    "moep_labels", "moep_loss", "moep_act_backward", "moep_optim_step", "moep_forward_train",
-    "moep_prefetch_plan", "moep_gather_rows",
-)
-
 vp = C.c_void_p
 i32, i64, f32, f64 = C.c_int32, C.c_int64, C.c_float, C.c_double
 
@@ -38,6 +32,7 @@ class PredictArgs(C.Structure):
         ("tau_abs", f32), ("tau_rel", f32), ("w2_norm", f32),
         ("ids", vp), ("logits", vp), ("flags", vp), ("flag_list", vp), ("flag_count", vp),
         ("truth", vp), ("k", i32), ("n_m", i32), ("m_list", i32 * MAX_BOUNDS), ("partials", vp),
+        ("a_out", vp),
     ]
 
 
@@ -46,11 +41,51 @@ class Fp64Args(C.Structure):
         ("n_tokens", i64), ("d", i32), ("hidden", i32), ("n_experts", i32), ("arch", i32),
         ("x_dtype", i32), ("w_dtype", i32),
         ("x", vp), ("w1", vp), ("b1", vp), ("bn_scale", vp), ("bn_shift", vp), ("bn_mean", vp),
-        ("bn_var", vp), ("bn_eps", f64), ("w2", vp), ("b2", vp),
+        ("bn_var", vp), ("bn_eps", f64), ("w2", vp), ("w2t", vp), ("b2", vp),
         ("rows", vp), ("row_count", vp), ("m_sel", i32), ("ids", vp), ("logits64", vp), ("logits32", vp),
         ("truth", vp), ("k", i32), ("n_m", i32), ("m_list", i32 * MAX_BOUNDS), ("partials", vp),
+        ("a_out", vp),
     ]
 
+
+class LossArgs(C.Structure):
+    _fields_ = [
+        ("family", i32),
+        ("top_weight", f64), ("mid_weight", f64), ("rest_weight", f64), ("ranking_lambda", f64),
+        ("margin", f64), ("focal_gamma", f64), ("focal_alpha", f64),
+        ("normalize_ranking", i32), ("n", i64), ("n_global", i64), ("n_experts", i32), ("dtype", i32),
+        ("logits", vp), ("scores", vp), ("rank_of", vp), ("topk_mask", vp), ("dz", vp), ("dz_hinge", vp),
+        ("partials", vp), ("n_blocks", i32),
+    ]
+
+
+class OptimArgs(C.Structure):
+    _fields_ = [
+        ("kind", i32), ("dtype", i32), ("n", i64), ("params", vp), ("grads", vp), ("m", vp), ("v", vp),
+        ("lr", f64), ("beta1", f64), ("beta2", f64), ("eps", f64), ("momentum", f64), ("t", i64),
+        ("shadow_bf16", vp), ("n_shadow", i64), ("nonfinite", vp),
+    ]
+
+
+# name -> argtypes (restype int32 unless listed in _RESTYPES)
+_SIGS = {
+    "moep_predict_bf16": [C.POINTER(PredictArgs), vp],
+    "moep_predict_fp64": [C.POINTER(Fp64Args), vp],
+    "moep_eval_logits": [vp, i32, i64, i32, vp, i32, i32, vp, vp, vp],
+    "moep_topk_logits": [vp, i32, i64, i32, i32, vp, vp],
+    "moep_rank_order": [vp, i32, i64, i32, vp, vp],
+    "moep_counters_reduce": [vp, i32, i32, vp, vp],
+    "moep_input_norm": [vp, i32, i64, i32, i32, vp, vp, f64, vp, vp, vp],
+    "moep_labels": [vp, i32, i64, i32, i32, vp, vp, vp, vp],
+    "moep_loss": [C.POINTER(LossArgs), vp],
+    "moep_loss_finalize": [vp, i32, i64, i32, i32, f64, i32, i32, vp, vp, vp, vp],
+    "moep_act_backward": [vp, vp, vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
+    "moep_optim_step": [C.POINTER(OptimArgs), vp],
+    "moep_num_sms": [],
+    "moep_version": [],
+}
+_RESTYPES = {"moep_version": C.c_char_p}
+EXPORTED = tuple(_SIGS)
 
 _lib = None
 
@@ -64,18 +99,10 @@ def lib():
                 f"{LIB_PATH} is missing: build it with `python -m paper_2511_10676_b200.build` "
                 "(there is no CPU fallback)")
         L = C.CDLL(LIB_PATH)
-        L.moep_predict_bf16.argtypes = [C.POINTER(PredictArgs), vp]
-        L.moep_predict_fp64.argtypes = [C.POINTER(Fp64Args), vp]
-        L.moep_eval_logits.argtypes = [vp, i32, i64, i32, vp, i32, i32, vp, vp, vp]
-        L.moep_topk_logits.argtypes = [vp, i32, i64, i32, i32, vp, vp]
-        L.moep_rank_order.argtypes = [vp, i32, i64, i32, vp, vp]
-        L.moep_counters_reduce.argtypes = [vp, i32, i32, vp, vp]
-        L.moep_input_norm.argtypes = [vp, i32, i64, i32, i32, vp, vp, f64, vp, vp, vp]
-        L.moep_num_sms.argtypes = []
-        L.moep_version.restype = C.c_char_p
-        for name in EXPORTED:
-            if hasattr(L, name):
-                getattr(L, name).restype = getattr(L, name).restype if name == "moep_version" else i32
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, i32)
         _lib = L
     return _lib
 
@@ -93,3 +120,8 @@ def check(rc: int, what: str) -> None:
 def ptr(t) -> int | None:
     """Raw device pointer of a torch tensor (None -> NULL)."""
     return None if t is None else t.data_ptr()
+
+
+def dtype_code(t) -> int:
+    import torch
+    return {torch.float64: MOEP_F64, torch.float32: MOEP_F32, torch.bfloat16: MOEP_BF16}[t.dtype]

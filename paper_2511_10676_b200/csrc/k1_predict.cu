@@ -73,6 +73,7 @@ struct Params {
   int m_list[MOEP_MAX_BOUNDS];
   int* partials;
   int n_counters;
+  float* a_out;
 };
 
 // ------------------------------------------------------------------ kernel
@@ -240,6 +241,7 @@ predict_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         // bias + activation + hi/lo split
         uint32_t hi2[32], lo2[32];
         const int col0 = c * HC + wg * 64;
+        const int64_t row_g = static_cast<int64_t>(tile) * BM + row_in_tile;
 #pragma unroll
         for (int j4 = 0; j4 < 16; ++j4) {
           float4 pa, pb;
@@ -253,6 +255,11 @@ predict_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
                                            : make_float4(0.f, 0.f, 0.f, 0.f);
           }
           const float ca[4] = {pa.x, pa.y, pa.z, pa.w};
+          if (ARCH == 2 && p.a_out && row_g < p.n_tokens && col0 + j4 * 4 < p.hidden) {
+            // training: keep the fp32 pre-activation for the backward pass
+            *reinterpret_cast<float4*>(p.a_out + row_g * p.hidden + col0 + j4 * 4) =
+                make_float4(v[j4 * 4] + pa.x, v[j4 * 4 + 1] + pa.y, v[j4 * 4 + 2] + pa.z, v[j4 * 4 + 3] + pa.w);
+          }
           float hv[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
@@ -510,7 +517,7 @@ int launch_k1(const moep_predict_args* a, cudaStream_t st, const CUtensorMap& tx
   p.tau_abs = a->tau_abs; p.tau_rel = a->tau_rel; p.w2_norm = a->w2_norm;
   p.ids = a->ids; p.logits = a->logits; p.flags = a->flags;
   p.flag_list = a->flag_list; p.flag_count = a->flag_count;
-  p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials;
+  p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;
   p.n_counters = moep_n_counters(a->n_m, a->n_experts);
   const int grid = moep_num_sms();
   kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);

@@ -1,0 +1,458 @@
+// train.cu — training kernels for the expert predictor.
+//
+//   K3 moep_labels          BatchLabels.from_scores (losses.py:64-74): stable
+//                           1-based ranks, top-k mask, strict-pair counts.
+//   K4 moep_loss            loss_and_grad (losses.py:243-273) for mse / wbce /
+//                           focal / ranking (three-tier WBCE + pairwise hinge),
+//                           one warp per token, per-CTA partial sums.
+//      moep_loss_finalize   global normalisers (N*E, batch n_pairs) -> dZ, loss.
+//   K5 moep_act_backward    dA = (dZ . W2) * act'(a), dW2 = dZ^T . act(a),
+//                           db1, db2 (predictor.py:261-297, arch2 branch);
+//                           column-parallel with deterministic split-N partials.
+//   K6 moep_optim_step      Adam / SGD / momentum with bias correction
+//                           (trainer.py:103-122) on a flat fp32 master buffer,
+//                           writing the bf16 shadow the forward GEMMs read and
+//                           a non-finite flag (trainer.py:125-128).
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "common.cuh"
+
+namespace moep {
+namespace tr {
+
+constexpr int NT = 256;
+
+template <typename T>
+__device__ __forceinline__ double ldd(const T* p, int64_t i) { return static_cast<double>(p[i]); }
+
+// ------------------------------------------------------------------ K3
+template <typename T>
+__global__ void __launch_bounds__(NT)
+labels_kernel(const T* __restrict__ s, int64_t n, int E, int k, int top_cut, int* __restrict__ rank_of,
+              uint8_t* __restrict__ mask, int* __restrict__ pairs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  for (int64_t row = gw; row < n; row += nw) {
+    const T* sr = s + row * E;
+    int np = 0;
+    for (int e = lane; e < E; e += 32) {
+      const double se = ldd(sr, e);
+      int r = 0;
+      for (int j = 0; j < E; ++j) r += key_gt(ldd(sr, j), j, se, e) ? 1 : 0;
+      rank_of[row * E + e] = r + 1;
+      mask[row * E + e] = r < k ? 1 : 0;
+    }
+    __syncwarp();
+    // strict pairs among the true top-T (losses.py:202-207)
+    for (int e = lane; e < E; e += 32) {
+      if (rank_of[row * E + e] <= top_cut) {
+        const double se = ldd(sr, e);
+        for (int j = 0; j < E; ++j)
+          if (rank_of[row * E + j] <= top_cut && se > ldd(sr, j)) ++np;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+    if (lane == 0 && pairs) pairs[row] = np;
+  }
+}
+
+// ------------------------------------------------------------------ K4
+struct LossParams {
+  int family;  // 0 mse, 1 wbce, 2 focal, 3 ranking
+  double top_w, mid_w, rest_w, lam, margin, gamma, alpha;
+  int top_cut, mid_cut;
+  double inv_ne;  // 1 / (N_global * E)
+  double inv_n;   // 1 / N_global
+};
+
+__device__ __forceinline__ double softplus(double v) {  // log(1 + e^v), stable (np.logaddexp(0, v))
+  return v > 0 ? v + log1p(exp(-v)) : log1p(exp(v));
+}
+__device__ __forceinline__ double sigm(double u) {
+  if (u >= 0.0) return 1.0 / (1.0 + exp(-u));
+  const double eu = exp(u);
+  return eu / (1.0 + eu);
+}
+
+// partials per CTA: [0] loss (bce/mse/focal part), [1] hinge total (unnormalised), [2] n_pairs
+template <typename T>
+__global__ void __launch_bounds__(NT)
+loss_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restrict__ rank_of,
+            const uint8_t* __restrict__ mask, int64_t n, int E, LossParams p, T* __restrict__ dz,
+            T* __restrict__ dz_hinge, double* __restrict__ partials) {
+  __shared__ double red[NT / 32][3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  double l_main = 0.0, l_hinge = 0.0, n_pairs = 0.0;
+  for (int64_t row = gw; row < n; row += nw) {
+    const T* zr = z + row * E;
+    const T* sr = s + row * E;
+    const int* rr = rank_of + row * E;
+    const uint8_t* mr = mask + row * E;
+    if (p.family == 0) {
+      // MSE on softmax probabilities (losses.py:99-110, chain rule :250-255)
+      double mx = -INFINITY;
+      for (int e = lane; e < E; e += 32) mx = fmax(mx, (double)zr[e]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      double se = 0.0;
+      for (int e = lane; e < E; e += 32) se += exp((double)zr[e] - mx);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+      double inner = 0.0;
+      for (int e = lane; e < E; e += 32) {
+        const double pr = exp((double)zr[e] - mx) / se;
+        const double diff = (double)sr[e] - pr;
+        l_main += diff * diff * p.inv_n;
+        inner += (-2.0 * diff * p.inv_n) * pr;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) inner += __shfl_xor_sync(0xffffffffu, inner, o);
+      for (int e = lane; e < E; e += 32) {
+        const double pr = exp((double)zr[e] - mx) / se;
+        const double dp = -2.0 * ((double)sr[e] - pr) * p.inv_n;
+        dz[row * E + e] = static_cast<T>(pr * (dp - inner));
+      }
+      continue;
+    }
+    for (int e = lane; e < E; e += 32) {
+      const double zv = zr[e];
+      const bool pos = mr[e] != 0;
+      if (p.family == 4) { dz[row * E + e] = T(0); continue; }  // hinge only
+      double g;
+      if (p.family == 2) {
+        // focal (losses.py:156-179)
+        const double log_pt = pos ? -softplus(-zv) : -softplus(zv);
+        const double pt = exp(log_pt);
+        const double at = pos ? p.alpha : 1.0 - p.alpha;
+        const double om = 1.0 - pt;
+        const double focus = pow(om, p.gamma);
+        l_main += -at * focus * log_pt * p.inv_ne;
+        const double sgn = pos ? 1.0 : -1.0;
+        g = at * sgn * (p.gamma * pt * focus * log_pt - pow(om, p.gamma + 1.0)) * p.inv_ne;
+      } else {
+        // tier weights (losses.py:113-121); three tiers only for the ranking family
+        const int r = rr[e];
+        double w = p.rest_w;
+        if (p.family == 3 && r > p.top_cut && r <= p.mid_cut) w = p.mid_w;
+        if (r <= p.top_cut) w = p.top_w;
+        const double lt = pos ? -softplus(-zv) : -softplus(zv);
+        l_main += -w * lt * p.inv_ne;
+        g = w * (sigm(zv) - (pos ? 1.0 : 0.0)) * p.inv_ne;
+      }
+      dz[row * E + e] = static_cast<T>(g);
+    }
+    if (p.family >= 3) {
+      // pairwise hinge over the true top-T (losses.py:182-217), unnormalised here
+      for (int e = lane; e < E; e += 32) {
+        double gh = 0.0;
+        if (rr[e] <= p.top_cut) {
+          const double se = sr[e], ze = zr[e];
+          for (int j = 0; j < E; ++j) {
+            if (j == e || rr[j] > p.top_cut) continue;
+            const double sj = sr[j], zj = zr[j];
+            if (se > sj) {  // e outranks j in truth: pair (e, j)
+              n_pairs += 1.0;
+              const double gap = p.margin - (ze - zj);
+              if (gap > 0) { l_hinge += gap; gh -= 1.0; }
+            } else if (sj > se) {  // pair (j, e)
+              const double gap = p.margin - (zj - ze);
+              if (gap > 0) gh += 1.0;
+            }
+          }
+        }
+        dz_hinge[row * E + e] = static_cast<T>(gh);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l_main += __shfl_xor_sync(0xffffffffu, l_main, o);
+    l_hinge += __shfl_xor_sync(0xffffffffu, l_hinge, o);
+    n_pairs += __shfl_xor_sync(0xffffffffu, n_pairs, o);
+  }
+  if (lane == 0) { red[warp][0] = l_main; red[warp][1] = l_hinge; red[warp][2] = n_pairs; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
+    partials[blockIdx.x * 3 + threadIdx.x] = v;
+  }
+}
+
+// sums partials in a fixed order; ranking: dz += lam/n_pairs * dz_hinge
+template <typename T>
+__global__ void finalize_kernel(const double* __restrict__ partials, int nblk, int64_t n, int E, int family,
+                                double lam, int normalize, T* __restrict__ dz,
+                                const T* __restrict__ dz_hinge, double* __restrict__ out_loss) {
+  __shared__ double tot[3];
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int b = 0; b < nblk; ++b) v += partials[b * 3 + threadIdx.x];
+    tot[threadIdx.x] = v;
+  }
+  __syncthreads();
+  double scale = 0.0;
+  if (family >= 3) {
+    double hinge = tot[1];
+    scale = lam;
+    if (normalize && tot[2] > 0) { hinge /= tot[2]; scale = lam / tot[2]; }
+    if (blockIdx.x == 0 && threadIdx.x == 0) { out_loss[0] = tot[0] + lam * hinge; out_loss[1] = tot[2]; }
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n * E;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      dz[i] = static_cast<T>(static_cast<double>(dz[i]) + scale * static_cast<double>(dz_hinge[i]));
+  } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out_loss[0] = tot[0];
+    out_loss[1] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------------ K5
+// One thread per hidden column j, a CTA covers 128 columns x a slice of rows.
+// Writes dA (fp32) and per-slice partials of dW2 [E, h], db1 [h], db2 [E].
+template <int EMAX, typename T>
+__global__ void __launch_bounds__(128)
+act_backward_kernel(const T* __restrict__ a, const T* __restrict__ dz, const T* __restrict__ w2,
+                    int64_t n, int H, int E, int rows_per_slice, T* __restrict__ da,
+                    T* __restrict__ dw2_part, T* __restrict__ db1_part, T* __restrict__ db2_part) {
+  __shared__ T sdz[32][EMAX];
+  const int j = blockIdx.x * 128 + threadIdx.x;
+  const int slice = blockIdx.y;
+  const int64_t r0 = static_cast<int64_t>(slice) * rows_per_slice;
+  const int64_t r1 = (r0 + rows_per_slice < n) ? r0 + rows_per_slice : n;
+  T w2c[EMAX], acc[EMAX];
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) {
+    w2c[e] = (j < H && e < E) ? w2[static_cast<int64_t>(e) * H + j] : T(0);
+    acc[e] = T(0);
+  }
+  T db1 = T(0);
+  for (int64_t rb = r0; rb < r1; rb += 32) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * EMAX; i += 128) {
+      const int rr = i / EMAX, e = i % EMAX;
+      sdz[rr][e] = (rb + rr < r1 && e < E) ? dz[(rb + rr) * E + e] : T(0);
+    }
+    __syncthreads();
+    if (j < H) {
+      const int lim = (r1 - rb < 32) ? static_cast<int>(r1 - rb) : 32;
+      for (int rr = 0; rr < lim; ++rr) {
+        const int64_t row = rb + rr;
+        const T av = a[row * H + j];
+        // branch-stable sigmoid (predictor.py:39-45), silu / silu' (:48-54)
+        T sg;
+        if (av >= T(0)) sg = T(1) / (T(1) + exp(-av));
+        else { const T ea = exp(av); sg = ea / (T(1) + ea); }
+        const T hv = av * sg;
+        const T dsilu = sg * (T(1) + av * (T(1) - sg));
+        T dh = T(0);
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+          dh = fma(sdz[rr][e], w2c[e], dh);
+          acc[e] = fma(sdz[rr][e], hv, acc[e]);
+        }
+        const T dav = dh * dsilu;
+        da[row * H + j] = dav;
+        db1 += dav;
+      }
+    }
+  }
+  if (j < H) {
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e)
+      if (e < E) dw2_part[(static_cast<int64_t>(slice) * E + e) * H + j] = acc[e];
+    db1_part[static_cast<int64_t>(slice) * H + j] = db1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < E) {
+    T s = T(0);
+    for (int64_t row = r0; row < r1; ++row) s += dz[row * E + threadIdx.x];
+    db2_part[static_cast<int64_t>(slice) * E + threadIdx.x] = s;
+  }
+}
+
+template <typename T>
+__global__ void sum_slices_kernel(const T* __restrict__ part, int nslice, int64_t len, T* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    T s = T(0);
+    for (int k = 0; k < nslice; ++k) s += part[k * len + i];
+    out[i] = s;
+  }
+}
+
+// ------------------------------------------------------------------ K6
+// Operation order follows trainer.py:109-122 (m *= b1; m += (1-b1) g; ...),
+// evaluated in T (fp64 for the exact-parity mode, fp32 master otherwise).
+template <typename T>
+__global__ void optim_kernel(T* __restrict__ p, const T* __restrict__ g, T* __restrict__ m,
+                             T* __restrict__ v, int64_t n, int kind, T lr, T b1, T b2, T eps,
+                             T bc1, T bc2, T mom, __nv_bfloat16* __restrict__ shadow,
+                             int64_t n_shadow, int* __restrict__ nonfinite) {
+  int bad = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const T gi = g[i];
+    T pi = p[i];
+    if (kind == 0) {          // sgd
+      pi -= lr * gi;
+    } else if (kind == 1) {   // momentum: m = mu*m + g ; p -= lr*m
+      T mi = m[i] * mom;
+      mi += gi;
+      m[i] = mi;
+      pi -= lr * mi;
+    } else {                  // adam with bias correction
+      T mi = m[i] * b1;
+      mi += (T(1) - b1) * gi;
+      T vi = v[i] * b2;
+      vi += (T(1) - b2) * gi * gi;
+      m[i] = mi;
+      v[i] = vi;
+      const T mh = mi / bc1, vh = vi / bc2;
+      pi -= lr * mh / (sqrt(vh) + eps);
+    }
+    p[i] = pi;
+    bad |= !isfinite(pi);
+    if (shadow && i < n_shadow) shadow[i] = __float2bfloat16_rn(static_cast<float>(pi));
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(nonfinite, 1);
+}
+
+}  // namespace tr
+}  // namespace moep
+
+using namespace moep::tr;
+
+extern "C" {
+
+int moep_labels(const void* scores, int32_t dtype, int64_t n, int32_t E, int32_t k, int32_t* rank_of,
+                uint8_t* topk_mask, int32_t* pair_count, void* stream) {
+  if (n <= 0 || E <= 0) return MOEP_ESHAPE;
+  if (k < 1 || k > E) return MOEP_EARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = moep_num_sms() * 4;
+  const int top_cut = E < 10 ? E : 10;  // TOP_TIER_SIZE (losses.py:27)
+  if (dtype == MOEP_F64)
+    labels_kernel<double><<<grid, NT, 0, st>>>(static_cast<const double*>(scores), n, E, k, top_cut, rank_of,
+                                                 topk_mask, pair_count);
+  else if (dtype == MOEP_F32)
+    labels_kernel<float><<<grid, NT, 0, st>>>(static_cast<const float*>(scores), n, E, k, top_cut, rank_of,
+                                                topk_mask, pair_count);
+  else
+    return MOEP_EARG;
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+int moep_loss(const moep_loss_args* a, void* stream) {
+  if (!a || a->n <= 0 || a->n_experts <= 0 || a->n_blocks <= 0) return MOEP_ESHAPE;
+  if (a->family < 0 || a->family > 4) return MOEP_EARG;
+  if (a->family >= 3 && !a->dz_hinge) return MOEP_EARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LossParams p;
+  p.family = a->family;
+  p.top_w = a->top_weight; p.mid_w = a->mid_weight; p.rest_w = a->rest_weight;
+  p.lam = a->ranking_lambda; p.margin = a->margin; p.gamma = a->focal_gamma; p.alpha = a->focal_alpha;
+  p.top_cut = a->n_experts < 10 ? a->n_experts : 10;
+  p.mid_cut = a->n_experts < 30 ? a->n_experts : 30;
+  p.inv_ne = 1.0 / (static_cast<double>(a->n_global) * a->n_experts);
+  p.inv_n = 1.0 / static_cast<double>(a->n_global);
+  if (a->dtype == MOEP_F64)
+    loss_kernel<double><<<a->n_blocks, NT, 0, st>>>(
+        static_cast<const double*>(a->logits), static_cast<const double*>(a->scores), a->rank_of, a->topk_mask,
+        a->n, a->n_experts, p, static_cast<double*>(a->dz), static_cast<double*>(a->dz_hinge), a->partials);
+  else if (a->dtype == MOEP_F32)
+    loss_kernel<float><<<a->n_blocks, NT, 0, st>>>(
+        static_cast<const float*>(a->logits), static_cast<const float*>(a->scores), a->rank_of, a->topk_mask,
+        a->n, a->n_experts, p, static_cast<float*>(a->dz), static_cast<float*>(a->dz_hinge), a->partials);
+  else
+    return MOEP_EARG;
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+int moep_loss_finalize(const double* partials, int32_t n_blocks, int64_t n, int32_t E, int32_t family,
+                       double ranking_lambda, int32_t normalize, int32_t dtype, void* dz, const void* dz_hinge,
+                       double* out_loss, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = family >= 3 ? moep_num_sms() : 1;
+  if (dtype == MOEP_F64)
+    finalize_kernel<double><<<grid, 256, 0, st>>>(partials, n_blocks, n, E, family, ranking_lambda, normalize,
+                                                  static_cast<double*>(dz), static_cast<const double*>(dz_hinge),
+                                                  out_loss);
+  else if (dtype == MOEP_F32)
+    finalize_kernel<float><<<grid, 256, 0, st>>>(partials, n_blocks, n, E, family, ranking_lambda, normalize,
+                                                 static_cast<float*>(dz), static_cast<const float*>(dz_hinge),
+                                                 out_loss);
+  else
+    return MOEP_EARG;
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+}  // extern "C"
+
+template <typename T>
+static int act_backward_t(const T* a, const T* dz, const T* w2, int64_t n, int32_t H, int32_t E, int32_t n_slices,
+                          T* da, T* dw2, T* db1, T* db2, T* scratch, cudaStream_t st) {
+  const int rows_per_slice = static_cast<int>((n + n_slices - 1) / n_slices);
+  T* dw2_part = scratch;
+  T* db1_part = dw2_part + static_cast<int64_t>(n_slices) * E * H;
+  T* db2_part = db1_part + static_cast<int64_t>(n_slices) * H;
+  dim3 grid((H + 127) / 128, n_slices);
+  if (E <= 16) act_backward_kernel<16, T><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, da, dw2_part, db1_part, db2_part);
+  else if (E <= 32) act_backward_kernel<32, T><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, da, dw2_part, db1_part, db2_part);
+  else if (E <= 64) act_backward_kernel<64, T><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, da, dw2_part, db1_part, db2_part);
+  else act_backward_kernel<128, T><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, da, dw2_part, db1_part, db2_part);
+  const int g2 = moep_num_sms() * 2;
+  sum_slices_kernel<T><<<g2, 256, 0, st>>>(dw2_part, n_slices, static_cast<int64_t>(E) * H, dw2);
+  sum_slices_kernel<T><<<g2, 256, 0, st>>>(db1_part, n_slices, H, db1);
+  sum_slices_kernel<T><<<1, 256, 0, st>>>(db2_part, n_slices, E, db2);
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+extern "C" {
+
+int moep_act_backward(const void* a, const void* dz, const void* w2, int32_t dtype, int64_t n, int32_t H,
+                      int32_t E, int32_t n_slices, void* da, void* dw2, void* db1, void* db2, void* scratch,
+                      void* stream) {
+  if (n <= 0 || H <= 0 || E <= 0 || n_slices <= 0) return MOEP_ESHAPE;
+  if (E > 128) return MOEP_EUNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == MOEP_F64)
+    return act_backward_t<double>(static_cast<const double*>(a), static_cast<const double*>(dz),
+                                  static_cast<const double*>(w2), n, H, E, n_slices, static_cast<double*>(da),
+                                  static_cast<double*>(dw2), static_cast<double*>(db1), static_cast<double*>(db2),
+                                  static_cast<double*>(scratch), st);
+  if (dtype == MOEP_F32)
+    return act_backward_t<float>(static_cast<const float*>(a), static_cast<const float*>(dz),
+                                 static_cast<const float*>(w2), n, H, E, n_slices, static_cast<float*>(da),
+                                 static_cast<float*>(dw2), static_cast<float*>(db1), static_cast<float*>(db2),
+                                 static_cast<float*>(scratch), st);
+  return MOEP_EARG;
+}
+
+int moep_optim_step(const moep_optim_args* a, void* stream) {
+  if (!a || a->n <= 0) return MOEP_ESHAPE;
+  if (a->kind < 0 || a->kind > 2) return MOEP_EARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // bias corrections as trainer.py:120-121 computes them: 1 - beta**t in float64
+  const double bc1 = 1.0 - pow(a->beta1, static_cast<double>(a->t));
+  const double bc2 = 1.0 - pow(a->beta2, static_cast<double>(a->t));
+  const int grid = moep_num_sms() * 4;
+  if (a->dtype == MOEP_F64)
+    optim_kernel<double><<<grid, 256, 0, st>>>(
+        static_cast<double*>(a->params), static_cast<const double*>(a->grads), static_cast<double*>(a->m),
+        static_cast<double*>(a->v), a->n, a->kind, a->lr, a->beta1, a->beta2, a->eps, bc1, bc2, a->momentum,
+        static_cast<__nv_bfloat16*>(a->shadow_bf16), a->n_shadow, a->nonfinite);
+  else if (a->dtype == MOEP_F32)
+    optim_kernel<float><<<grid, 256, 0, st>>>(
+        static_cast<float*>(a->params), static_cast<const float*>(a->grads), static_cast<float*>(a->m),
+        static_cast<float*>(a->v), a->n, a->kind, static_cast<float>(a->lr), static_cast<float>(a->beta1),
+        static_cast<float>(a->beta2), static_cast<float>(a->eps), static_cast<float>(bc1), static_cast<float>(bc2),
+        static_cast<float>(a->momentum), static_cast<__nv_bfloat16*>(a->shadow_bf16), a->n_shadow, a->nonfinite);
+  else
+    return MOEP_EARG;
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+}  // extern "C"

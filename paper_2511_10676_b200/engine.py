@@ -102,6 +102,9 @@ class DevicePredictor:
         self.w2_bf16 = w2.to(torch.bfloat16).contiguous()
         self.w1_f64 = None if self.weights_bf16_exact else w1
         self.w2_f64 = None if self.weights_bf16_exact else w2
+        # K2 reads W2 transposed ([h, E]) so lanes stream consecutive experts
+        self.w2t_bf16 = self.w2_bf16.t().contiguous()
+        self.w2t_f64 = None if self.weights_bf16_exact else w2.t().contiguous()
         self.b1_f64, self.b2_f64 = f64(model.b1), f64(model.b2)
         self.b1_f32, self.b2_f32 = self.b1_f64.float(), self.b2_f64.float()
         self.bn_eps = float(getattr(model, "bn_eps", 1e-5))
@@ -179,6 +182,7 @@ class DevicePredictor:
         a.x = ptr(x)
         a.w1 = ptr(self.w1_bf16 if exact_w else self.w1_f64)
         a.w2 = ptr(self.w2_bf16 if exact_w else self.w2_f64)
+        a.w2t = ptr(self.w2t_bf16 if exact_w else self.w2t_f64)
         a.b1, a.b2 = ptr(self.b1_f64), ptr(self.b2_f64)
         a.bn_scale, a.bn_shift, a.bn_mean, a.bn_var = (ptr(t) for t in self.bn)
         a.bn_eps = self.bn_eps

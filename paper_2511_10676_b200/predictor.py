@@ -166,6 +166,54 @@ def predict_topk(model: PredictorModel, x, m: int) -> ExpertSelection:
     return ExpertSelection(indices=ids.astype(np.int64), raw_scores=logits)
 
 
+def _trainer_fp64(model):
+    from .losses import LossSpec
+    from .train_engine import DeviceTrainer
+    if model.arch != "arch2":
+        raise NotImplementedError("device forward/backward in train mode is implemented for arch2 "
+                                  "(arch1 batch-norm training is listed as a gap in DESIGN.md)")
+    return DeviceTrainer(model, LossSpec(), precision="fp64")
+
+
+def forward(model: PredictorModel, x, *, dropout_mask=None):
+    """Predictor logits (predictor.py:243-258). Eval mode == predict_logits; train
+    mode runs the fp64 device forward (K2 with pre-activation output) and keeps
+    the intermediates for a paired backward()."""
+    if model.mode != "train":
+        return predict_logits(model, x)
+    batch, single, is_t = _as_batch(model, x)
+    tr = _trainer_fp64(model)
+    z, a_pre, xd = tr.forward(batch.to("cuda"))
+    host_x = batch.detach().cpu().numpy().astype(np.float64) if is_t else batch.numpy()
+    model._cache = {"x": host_x, "a": a_pre, "x_dev": xd, "trainer": tr}
+    out = z if is_t else z.cpu().numpy()
+    return out[0] if single else out
+
+
+def backward(model: PredictorModel, x, dlogits) -> dict:
+    """Parameter gradients from upstream d(loss)/d(logits) (predictor.py:300-327),
+    fp64 on the device: K5 for the activation / W2 / bias terms, an fp64 GEMM for dW1."""
+    batch, single, is_t = _as_batch(model, x)
+    dz = dlogits if isinstance(dlogits, torch.Tensor) else torch.as_tensor(np.asarray(dlogits, dtype=np.float64))
+    dz = dz.to("cuda", torch.float64)
+    if single:
+        dz = dz[None]
+    if tuple(dz.shape) != (batch.shape[0], model.n_experts):
+        raise ConfigurationError(f"upstream gradient shape {tuple(dz.shape)} mismatches logits")
+    if model.mode == "train":
+        c = model._cache
+        host_x = batch.detach().cpu().numpy().astype(np.float64) if is_t else batch.numpy()
+        if c is None or c["x"].shape != host_x.shape or not np.array_equal(c["x"], host_x):
+            raise UsageError("train-mode backward requires a paired forward on the same input")
+        tr, a_pre, xd = c["trainer"], c["a"], c["x_dev"]
+    else:
+        tr = _trainer_fp64(model)
+        _, a_pre, xd = tr.forward(batch.to("cuda"))
+    tr.backward(xd, a_pre, dz.contiguous())
+    names = ("w1", "w2", "b1", "b2")
+    return {n: tr.view(tr.grad, i).clone().cpu().numpy() for i, n in enumerate(names)}
+
+
 def save_model(model: PredictorModel, path) -> None:
     """MOEPM1 checkpoint, float64 parameters in fixed order (predictor.py:354-369)."""
     arrays = [model.w1, model.b1, model.w2, model.b2]

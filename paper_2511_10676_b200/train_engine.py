@@ -1,0 +1,164 @@
+"""Device training state for an arch2 predictor (one GPU, optional DP hooks).
+
+Parameters live in one flat master buffer [w1 | w2 | b1 | b2] (the layout the
+fused optimizer K6 walks), with gradients, Adam moments and — in fp32 mode —
+a bf16 shadow of [w1 | w2] that the tensor-core forward (K1) reads.
+
+Two precision modes:
+  "fp64"  exact-parity mode: forward K2 (fp64 CUDA cores, fp64 pre-activations),
+          K4 loss in fp64, K5 fp64, dW1 by an fp64 GEMM, K6 in fp64 — the
+          reference's float64 arithmetic (trainer.py:131-204) step for step.
+  "fp32"  throughput mode: forward K1 (bf16 tcgen05 GEMMs with the hi/lo GEMM2,
+          fp32 pre-activations), K4 on fp32 logits (fp64 math), K5 fp32,
+          dW1 = dA^T X on bf16 tensor cores with dA split hi+lo (fp32 out),
+          fp32 master weights + Adam moments.
+One step = forward, loss (+ optional all-reduce of the 3 loss partials for
+batch-global normalisers), backward, optional gradient all-reduce, optimizer.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import MOEP_BF16, MOEP_F64, check, dtype_code, lib, ptr
+from .exceptions import ConfigurationError
+from .losses import LossSpec, device_loss
+
+OPT_KIND = {"sgd": 0, "momentum": 1, "adam": 2}
+
+
+def _stream(dev):
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+class DeviceTrainer:
+    def __init__(self, model, loss: LossSpec, optimizer="adam", lr=1e-3, momentum=0.9, beta1=0.9,
+                 beta2=0.999, eps=1e-8, precision="fp32", device="cuda", grad_allreduce=None,
+                 loss_allreduce=None):
+        if model.arch != "arch2":
+            raise ConfigurationError("device training supports arch2 predictors (arch1 BN-train: see DESIGN.md)")
+        if precision not in ("fp32", "fp64"):
+            raise ConfigurationError(f"unknown precision {precision!r}")
+        self.dev = torch.device(device)
+        lib()
+        self.loss_spec, self.kind = loss, OPT_KIND[optimizer]
+        self.lr, self.momentum, self.beta1, self.beta2, self.eps = lr, momentum, beta1, beta2, eps
+        self.precision = precision
+        self.dt = torch.float64 if precision == "fp64" else torch.float32
+        self.d, self.H, self.E = model.d, model.hidden, model.n_experts
+        d, H, E = self.d, self.H, self.E
+        self.sizes = [H * d, E * H, H, E]
+        self.offs = np.concatenate([[0], np.cumsum(self.sizes)]).tolist()
+        n = self.offs[-1]
+        self.flat = torch.empty(n, dtype=self.dt, device=self.dev)
+        for arr, o, s in zip((model.w1, model.w2, model.b1, model.b2), self.offs, self.sizes):
+            self.flat[o: o + s].copy_(torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float64).ravel()))
+        self.grad = torch.zeros_like(self.flat)
+        self.m = torch.zeros_like(self.flat)
+        self.v = torch.zeros_like(self.flat) if self.kind == 2 else None
+        self.n_shadow = H * d + E * H
+        self.shadow = None
+        if precision == "fp32":
+            self.shadow = self.flat[: self.n_shadow].to(torch.bfloat16)
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.t = 0
+        self.grad_allreduce, self.loss_allreduce = grad_allreduce, loss_allreduce
+        self.n_sms = lib().moep_num_sms()
+
+    # ------------------------------------------------------------ views
+    def view(self, buf, i):
+        shapes = [(self.H, self.d), (self.E, self.H), (self.H,), (self.E,)]
+        return buf[self.offs[i]: self.offs[i] + self.sizes[i]].view(shapes[i])
+
+    def params_numpy(self):
+        return [self.view(self.flat, i).double().cpu().numpy() for i in range(4)]
+
+    # ---------------------------------------------------------- forward
+    def forward(self, x):
+        """Train-mode arch2 forward: logits [N, E] and pre-activations a [N, H]."""
+        n = x.shape[0]
+        if self.precision == "fp32":
+            xb = x if x.dtype == torch.bfloat16 else x.to(torch.bfloat16)
+            z = torch.empty((n, self.E), dtype=torch.float32, device=self.dev)
+            a_pre = torch.empty((n, self.H), dtype=torch.float32, device=self.dev)
+            flags = torch.empty(n, dtype=torch.uint8, device=self.dev)
+            fl = torch.empty(n, dtype=torch.int32, device=self.dev)
+            fc = torch.zeros(1, dtype=torch.int32, device=self.dev)
+            A = _lib.PredictArgs()
+            A.n_tokens, A.d, A.hidden, A.n_experts, A.arch = n, self.d, self.H, self.E, 2
+            A.x = ptr(xb)
+            A.w1 = ptr(self.shadow[: self.H * self.d])
+            A.w2 = ptr(self.shadow[self.H * self.d:])
+            A.b1, A.b2 = ptr(self.view(self.flat, 2)), ptr(self.view(self.flat, 3))
+            A.logits, A.flags, A.flag_list, A.flag_count, A.a_out = ptr(z), ptr(flags), ptr(fl), ptr(fc), ptr(a_pre)
+            check(lib().moep_predict_bf16(A, _stream(self.dev)), "moep_predict_bf16")
+            return z, a_pre, xb
+        x64 = x if x.dtype in (torch.float64, torch.bfloat16) else x.to(torch.float64)
+        z = torch.empty((n, self.E), dtype=torch.float64, device=self.dev)
+        a_pre = torch.empty((n, self.H), dtype=torch.float64, device=self.dev)
+        w2t = self.view(self.flat, 1).t().contiguous()
+        A = _lib.Fp64Args()
+        A.n_tokens, A.d, A.hidden, A.n_experts, A.arch = n, self.d, self.H, self.E, 2
+        A.x_dtype, A.w_dtype = dtype_code(x64), MOEP_F64
+        A.x, A.w1, A.w2, A.w2t = ptr(x64), ptr(self.view(self.flat, 0)), ptr(self.view(self.flat, 1)), ptr(w2t)
+        A.b1, A.b2 = ptr(self.view(self.flat, 2)), ptr(self.view(self.flat, 3))
+        A.logits64, A.a_out = ptr(z), ptr(a_pre)
+        check(lib().moep_predict_fp64(A, _stream(self.dev)), "moep_predict_fp64")
+        return z, a_pre, x64
+
+    # --------------------------------------------------------- backward
+    def backward(self, x_used, a_pre, dz):
+        """K5 (activation backward + dW2/db1/db2) and the dW1 GEMM into self.grad."""
+        n = x_used.shape[0]
+        H, E = self.H, self.E
+        n_slices = max(1, min(64, n // 256))
+        da = torch.empty((n, H), dtype=self.dt, device=self.dev)
+        scratch = torch.empty(n_slices * (E * H + H + E), dtype=self.dt, device=self.dev)
+        check(lib().moep_act_backward(ptr(a_pre), ptr(dz), ptr(self.view(self.flat, 1)), dtype_code(dz), n, H, E,
+                                      n_slices, ptr(da), ptr(self.view(self.grad, 1)), ptr(self.view(self.grad, 2)),
+                                      ptr(self.view(self.grad, 3)), ptr(scratch), _stream(self.dev)),
+              "moep_act_backward")
+        gw1 = self.view(self.grad, 0)
+        if self.precision == "fp64":
+            xs = x_used if x_used.dtype == torch.float64 else x_used.to(torch.float64)
+            torch.mm(da.t(), xs, out=gw1)  # plain fp64 GEMM (cuBLAS DGEMM)
+        else:
+            # dW1 = dA^T X on bf16 tensor cores: dA split hi + lo, fp32 accumulate/output
+            hi = da.to(torch.bfloat16)
+            lo = (da - hi.float()).to(torch.bfloat16)
+            a2 = torch.cat([hi, lo], dim=0)                    # [2n, H]
+            x2 = torch.cat([x_used, x_used], dim=0)            # [2n, d] bf16 (exact inputs)
+            gw1.copy_(torch.mm(a2.t(), x2, out_dtype=torch.float32))
+        return da
+
+    # -------------------------------------------------------------- step
+    def optimizer_step(self):
+        self.t += 1
+        A = _lib.OptimArgs()
+        A.kind, A.dtype, A.n = self.kind, dtype_code(self.flat), self.flat.numel()
+        A.params, A.grads, A.m, A.v = ptr(self.flat), ptr(self.grad), ptr(self.m), ptr(self.v)
+        A.lr, A.beta1, A.beta2, A.eps, A.momentum, A.t = self.lr, self.beta1, self.beta2, self.eps, self.momentum, self.t
+        A.shadow_bf16, A.n_shadow, A.nonfinite = ptr(self.shadow), self.n_shadow, ptr(self.nonfinite)
+        check(lib().moep_optim_step(A, _stream(self.dev)), "moep_optim_step")
+
+    def step(self, x, scores, mask, rank, n_global=None):
+        """One training step; returns the device loss tensor [loss, n_pairs] (no host sync)."""
+        z, a_pre, x_used = self.forward(x)
+        zs = z if scores.dtype == z.dtype else z.to(scores.dtype)
+        out, dz = device_loss(self.loss_spec, zs, scores, mask, rank, n_global=n_global,
+                              allreduce=self.loss_allreduce)
+        if dz.dtype != self.dt:
+            dz = dz.to(self.dt)
+        self.backward(x_used, a_pre, dz)
+        if self.grad_allreduce is not None:
+            self.grad_allreduce(self.grad)
+        self.optimizer_step()
+        return out
+
+    def to_model(self, template):
+        from .predictor import PredictorModel
+        w1, w2, b1, b2 = self.params_numpy()
+        return PredictorModel("arch2", w1, b1, w2, b2, dropout_rate=template.dropout_rate,
+                              dropout_seed=template.dropout_seed)

@@ -71,3 +71,24 @@ int main(){{printf("%zu %zu %zu %zu\\n", sizeof(moep_predict_args), offsetof(moe
     got = [int(v) for v in subprocess.run([tmp], capture_output=True, text=True).stdout.split()]
     assert got == [ctypes.sizeof(_lib.PredictArgs), _lib.PredictArgs.partials.offset,
                    ctypes.sizeof(_lib.Fp64Args), _lib.Fp64Args.partials.offset]
+
+
+def test_loss_and_optim_struct_layouts(libpath):
+    from paper_2511_10676_b200 import _lib
+    src = f'''#include "{HEADER}"
+#include <stdio.h>
+#include <stddef.h>
+int main(){{printf("%zu %zu %zu %zu\\n", sizeof(moep_loss_args), offsetof(moep_loss_args, n_blocks),
+ sizeof(moep_optim_args), offsetof(moep_optim_args, nonfinite));return 0;}}'''
+    tmp = "/tmp/moep_layout_probe2"
+    with open(tmp + ".c", "w") as f:
+        f.write(src)
+    subprocess.run(["gcc", "-o", tmp, tmp + ".c"], check=True)
+    got = [int(v) for v in subprocess.run([tmp], capture_output=True, text=True).stdout.split()]
+    assert got == [ctypes.sizeof(_lib.LossArgs), _lib.LossArgs.n_blocks.offset,
+                   ctypes.sizeof(_lib.OptimArgs), _lib.OptimArgs.nonfinite.offset]
+
+
+def test_python_binding_covers_header():
+    from paper_2511_10676_b200 import _lib
+    assert set(declared_symbols()) == set(_lib.EXPORTED)

@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference's golden fixtures. Bit-exact for ids / counters; logits within the
+stated tolerance (1e-5 absolute for the bf16 tensor-core path before fix-up,
+exact-fp64 rows after)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_ATOL_K1 = 2e-5  # raw K1 logits vs fp64 (tensor-core fp32 accumulation, truncating)
+
+
+@pytest.fixture(scope="module")
+def pb():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2511_10676_b200 as pb
+    return pb
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import oracle
+    return oracle
+
+
+def bf16_model(pb, O, arch, d, h, e, seed, rng=None):
+    m = pb.init_model(arch, d, h, e, seed=seed)
+    m.w1 = O.round_bf16(m.w1)
+    m.w2 = O.round_bf16(m.w2)
+    if arch == "arch1" and rng is not None:
+        m.bn_mean = rng.standard_normal(h) * 0.05
+        m.bn_var = 0.3 + rng.random(h) * 0.5
+        m.bn_scale = 1 + 0.1 * rng.standard_normal(h)
+        m.bn_shift = 0.1 * rng.standard_normal(h)
+    return m
+
+
+def oracle_params(m):
+    p = {"arch": m.arch, "w1": m.w1, "b1": m.b1, "w2": m.w2, "b2": m.b2}
+    if m.arch == "arch1":
+        p.update(bn_scale=m.bn_scale, bn_shift=m.bn_shift, bn_mean=m.bn_mean, bn_var=m.bn_var)
+    return p
+
+
+# ------------------------------------------------------------- goldens
+@pytest.mark.parametrize("arch", ["arch1", "arch2"])
+def test_small_reference_shapes_golden(pb, golden, arch):
+    """d=8, h=16, E=8 perturbed models from the reference tests (fp64 weights -> K2 path)."""
+    g = golden("predictor")
+    pre = f"small_{arch}_"
+    kw = {n: g[pre + n] for n in ("bn_scale", "bn_shift", "bn_mean", "bn_var")} if arch == "arch1" else {}
+    m = pb.PredictorModel(arch, g[pre + "w1"], g[pre + "b1"], g[pre + "w2"], g[pre + "b2"], **kw)
+    z = pb.predict_logits(m, g[pre + "x"])
+    assert np.allclose(z, g[pre + "logits"], rtol=0, atol=1e-12)
+    assert np.array_equal(pb.predict_topk_batch(m, g[pre + "x"], 3), g[pre + "top3"])
+
+
+def test_c1_golden_ids(pb, golden, O):
+    """bf16-representable C1 layer: K1 tensor-core path + fix-up equals the reference."""
+    g = golden("predictor")
+    m = bf16_model(pb, O, "arch2", 2048, 2048, 64, seed=0)
+    x = g["c1_x"].astype(np.float64)
+    assert np.array_equal(pb.predict_topk_batch(m, x, 6), g["c1_top6"])
+    assert np.array_equal(pb.predict_topk_batch(m, x, 10), g["c1_top10"])
+    z = pb.predict_logits(m, x)
+    assert np.abs(z - g["c1_logits"]).max() < LOGIT_ATOL_K1
+
+
+def test_topk_golden(pb, golden):
+    g = golden("topk")
+    for k in (1, 3, 6, 11):
+        assert np.array_equal(pb.top_k_batch(g["tie_scores"], k), g[f"tie_top{k}"])
+    for k in (1, 6, 10, 64):
+        assert np.array_equal(pb.top_k_batch(g["rand_scores"], k), g[f"rand_top{k}"])
+    assert np.array_equal(pb.rank_order(g["rand_scores"]), g["rand_order"])
+
+
+def test_topk_hand_cases(pb):
+    # test_core.py:60-64, 78-79 + signed zero ties
+    assert pb.top_k(np.array([0.1, 0.7, 0.2]), 1).tolist() == [1]
+    assert pb.top_k(np.array([0.5, 0.5, 0.0]), 1).tolist() == [0]
+    assert pb.top_k(np.array([0.4, 0.1, 0.3, 0.2]), 2).tolist() == [0, 2]
+    assert pb.top_k(np.array([-0.0, 0.0, -1.0]), 1).tolist() == [0]
+    with pytest.raises(ValueError):
+        pb.top_k(np.array([1.0, 2.0]), 3)
+
+
+def test_eval_logits_golden(pb, golden):
+    from paper_2511_10676_b200.engine import EvalCounters, eval_logits_device
+    g = golden("metrics")
+    for idx in range(4):
+        pre = f"m{idx}_"
+        z, truth = g[pre + "z"], g[pre + "truth"]
+        n, e = z.shape
+        k = truth.shape[1]
+        ms = g[pre + "m_list"].tolist()
+        c = eval_logits_device(torch.from_numpy(z).cuda(), torch.from_numpy(truth), k, e, ms).cpu().numpy()
+        ec = EvalCounters.from_array(c, k, e, ms)
+        assert ec.overprov[k] / n == float(g[pre + "exact"])
+        assert ec.top1 / n == float(g[pre + "top1"])
+        assert [ec.overprov[m] / n for m in ms] == g[pre + "overprov"].tolist()
+        assert [ec.recall[m] / (n * k) for m in ms] == g[pre + "recall"].tolist()
+        assert np.array_equal(ec.per_expert_hits, g[pre + "hits"])
+        assert np.array_equal(ec.per_expert_truth, g[pre + "truthc"])
+
+
+# ---------------------------------------------- seeded parity vs the oracle
+CONFIGS = [
+    # (arch, d, h, E, k, n)    C1/C2 DSV2L, C3 Qwen3, C4 Phi (inference), arch1
+    ("arch2", 2048, 2048, 64, 6, 16384),
+    ("arch2", 2048, 2048, 128, 8, 8192),
+    ("arch2", 4096, 2048, 16, 2, 8192),
+    ("arch1", 2048, 2048, 64, 6, 4096),
+    ("arch2", 64, 128, 16, 2, 3000),     # ragged token count, small dims
+    ("arch2", 8, 16, 8, 2, 257),         # reference test dims through the tensor-core path
+]
+
+
+@pytest.mark.parametrize("arch,d,h,e,k,n", CONFIGS)
+def test_k1_ids_and_counters_vs_oracle(pb, O, arch, d, h, e, k, n):
+    rng = np.random.default_rng(d * 7 + e)
+    m = bf16_model(pb, O, arch, d, h, e, seed=3, rng=rng)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref = O.predict_logits(oracle_params(m), x)
+    dev = m.to_device()
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    assert dev.k1_usable(True, (k,))
+    for mm in sorted({1, k, min(k + 4, e)}):
+        if mm <= 15 or mm == e:
+            ids, flags = dev.topk(xt, mm, return_flags=True)
+            assert np.array_equal(ids.cpu().numpy(), O.top_k_batch(zref, mm)), mm
+    z = dev.logits(xt).cpu().numpy()
+    assert np.abs(z - zref).max() < LOGIT_ATOL_K1
+    truth = O.top_k_batch(zref + 0.05 * rng.standard_normal(zref.shape), k)  # correlated truth
+    ms = O.default_m_list(k, e)
+    cnt, fcount, _ = dev.evaluate(xt, torch.from_numpy(truth), k, ms)
+    c = pb.EvalCounters.from_array(cnt.cpu().numpy(), k, e, sorted(set(ms) | {k}))
+    oc = O.eval_counters(zref, truth, e, ms)
+    assert c.n == oc["n"] and c.top1 == oc["top1_count"]
+    assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
+    assert np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
+    assert np.array_equal(c.per_expert_truth, oc["per_expert_truth"])
+
+
+def test_margin_covers_error(pb, O):
+    """Calibration guard: raw K1 error / row scale stays well inside tau_rel."""
+    from paper_2511_10676_b200.engine import TAU_REL
+    rng = np.random.default_rng(11)
+    n, d, h, e = 16384, 2048, 2048, 64
+    m = bf16_model(pb, O, "arch2", d, h, e, seed=5)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref, cache = O.forward_eval(oracle_params(m), x)
+    dev = m.to_device()
+    lg = torch.empty((n, e), dtype=torch.float32, device="cuda")
+    dev._k1(torch.from_numpy(x).to("cuda", torch.bfloat16), logits=lg)
+    err = np.abs(lg.double().cpu().numpy() - zref).max(axis=1)
+    scale = np.linalg.norm(cache["h"], axis=1) * np.linalg.norm(m.w2, axis=1).max()
+    ratio = err / scale
+    # a decision flips only if two errors add up to delta: require 2*max < tau
+    assert 2 * ratio.max() < TAU_REL, ratio.max()
+
+
+def test_ties_go_to_fp64_and_lower_index(pb, O):
+    """Duplicate W2 rows give exact logit ties; the lower expert index must win."""
+    rng = np.random.default_rng(3)
+    m = bf16_model(pb, O, "arch2", 256, 256, 16, seed=9)
+    m.w2[5] = m.w2[2]
+    m.w2[9] = m.w2[2]
+    x = O.round_bf16(rng.standard_normal((512, 256)))
+    zref = O.predict_logits(oracle_params(m), x)
+    for mm in (1, 2, 3, 4):
+        assert np.array_equal(pb.predict_topk_batch(m, x, mm), O.top_k_batch(zref, mm))
+
+
+def test_nonfinite_input_raises(pb, O):
+    m = bf16_model(pb, O, "arch2", 64, 128, 16, seed=1)
+    x = np.zeros((4, 64))
+    x[2, 3] = np.nan
+    with pytest.raises(pb.ConfigurationError):
+        pb.predict_logits(m, x)
+    with pytest.raises(pb.ConfigurationError):
+        pb.predict_logits(m, np.zeros((4, 65)))
+
+
+def test_single_vector_and_m_range(pb, O):
+    m = bf16_model(pb, O, "arch2", 64, 128, 16, seed=1)
+    x = O.round_bf16(np.random.default_rng(0).standard_normal(64))
+    z = pb.predict_logits(m, x)
+    assert z.shape == (16,)
+    sel = pb.predict_topk(m, x, 4)
+    assert sel.indices.tolist() == O.top_k(O.predict_logits(oracle_params(m), x[None])[0], 4).tolist()
+    with pytest.raises(ValueError):
+        pb.predict_topk_batch(m, x[None], 17)
+    m.train()
+    with pytest.raises(pb.UsageError):
+        pb.predict_topk(m, x, 1)
+
+
+def test_non_bf16_inputs_take_exact_fp64_path(pb, O):
+    rng = np.random.default_rng(2)
+    m = pb.init_model("arch2", 64, 96, 16, seed=4)  # fp64 weights, not bf16-representable
+    x = rng.standard_normal((300, 64))
+    zref = O.predict_logits(oracle_params(m), x)
+    assert np.allclose(pb.predict_logits(m, x), zref, rtol=0, atol=1e-12)
+    for mm in (1, 2, 7, 16):
+        assert np.array_equal(pb.predict_topk_batch(m, x, mm), O.top_k_batch(zref, mm))
+
+
+def test_input_norm_kernel(pb, O):
+    rng = np.random.default_rng(5)
+    x = 3 * rng.standard_normal((64, 2048)) + 0.5
+    gamma = rng.uniform(0.5, 1.5, 2048)
+    beta = 0.1 * rng.standard_normal(2048)
+    m = bf16_model(pb, O, "arch2", 2048, 2048, 64, seed=0)
+    dev = m.to_device()
+    xt = torch.from_numpy(x).cuda()
+    for kind, g, b in (("rmsnorm", gamma, None), ("layernorm", gamma, beta), ("layernorm", None, None)):
+        out = dev.normalize(xt, kind, g, b).double().cpu().numpy()
+        ref = O.input_norm_bf16(x, kind, g, b)
+        assert np.array_equal(out, ref), kind

@@ -1,0 +1,144 @@
+"""GPU parity of the training path: labels (K3) and all loss families (K4)
+against the reference goldens, fp64 backward (K5 + fp64 GEMM) and optimizer
+(K6), a whole fp64 train() against the oracle's restated loop, and the fp32
+tensor-core mode within its stated tolerance."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2511_10676_b200 as pb
+    return pb
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import oracle
+    return oracle
+
+
+def test_labels_and_losses_golden(pb, golden):
+    g = golden("losses")
+    for n, e, k in ((4, 8, 2), (16, 16, 2), (8, 64, 6)):
+        pre = f"n{n}e{e}k{k}_"
+        lab = pb.BatchLabels.from_scores(g[pre + "scores"], k)
+        assert np.array_equal(lab.rank_of, g[pre + "rank_of"])
+        assert np.array_equal(lab.topk_mask, g[pre + "mask"])
+        for fam in ("mse", "wbce", "focal", "ranking"):
+            loss, grad = pb.loss_and_grad(pb.LossSpec(family=fam), g[pre + "z"], lab)
+            assert loss == pytest.approx(float(g[pre + fam + "_loss"]), rel=1e-12, abs=1e-15), fam
+            assert np.allclose(grad, g[pre + fam + "_grad"], rtol=1e-10, atol=1e-15), fam
+        _, _, n_pairs = pb.ranking_hinge(g[pre + "z"], lab)
+        assert n_pairs == int(g[pre + "n_pairs"])
+
+
+def test_loss_known_answers(pb):
+    lab = pb.BatchLabels.from_scores(np.array([[0.9, 0.1]]), 1)
+    loss, _ = pb.weighted_bce_loss(np.zeros((1, 2)), lab)
+    assert loss == pytest.approx(3.0 * np.log(2.0), abs=1e-12)  # test_losses.py:78-83
+    lab = pb.BatchLabels.from_scores(np.array([[0.7, 0.3]]), 1)
+    h, _, n_pairs = pb.ranking_hinge(np.ones((1, 2)), lab, margin=0.1)
+    assert n_pairs == 1 and h == pytest.approx(0.1)  # test_losses.py:133-137
+    lab = pb.BatchLabels(np.array([[0.4, 0.4, 0.2]]), np.array([[True, True, False]]), np.array([[1, 2, 3]]))
+    assert pb.ranking_hinge(np.zeros((1, 3)), lab)[2] == 2  # tie exclusion, test_losses.py:159-168
+
+
+def test_backward_golden_arch2(pb, golden):
+    g = golden("predictor")
+    pre = "small_arch2_"
+    m = pb.PredictorModel("arch2", g[pre + "w1"], g[pre + "b1"], g[pre + "w2"], g[pre + "b2"])
+    grads = pb.backward(m, g[pre + "x"], g[pre + "dz"])
+    for name in ("w1", "b1", "w2", "b2"):
+        assert np.allclose(grads[name], g[pre + "grad_" + name], rtol=1e-10, atol=1e-12), name
+
+
+def test_train_forward_backward_paired(pb, rng):
+    m = pb.init_model("arch2", 8, 16, 8, seed=7)
+    m.train()
+    x = rng.standard_normal((4, 8))
+    with pytest.raises(pb.UsageError):
+        pb.backward(m, x, np.ones((4, 8)))
+    pb.forward(m, x)
+    with pytest.raises(pb.UsageError):
+        pb.backward(m, rng.standard_normal((4, 8)), np.ones((4, 8)))
+    g = pb.backward(m, x, np.zeros((4, 8)))
+    assert all(np.all(v == 0) for v in g.values())
+
+
+def test_optimizer_golden(pb, golden):
+    from paper_2511_10676_b200 import _lib
+    g = golden("optim")
+    for opt, lr, kind in (("adam", 1e-3, 2), ("sgd", 0.05, 0), ("momentum", 0.02, 1)):
+        p = torch.as_tensor(np.concatenate([g["p0_w"].ravel(), g["p0_b"]])).cuda()
+        m = torch.zeros_like(p)
+        v = torch.zeros_like(p)
+        bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+        for t in range(3):
+            gr = torch.as_tensor(np.concatenate([g[f"{opt}_g{t}_w"].ravel(), g[f"{opt}_g{t}_b"]])).cuda()
+            a = _lib.OptimArgs()
+            a.kind, a.dtype, a.n = kind, _lib.MOEP_F64, p.numel()
+            a.params, a.grads, a.m, a.v = p.data_ptr(), gr.data_ptr(), m.data_ptr(), v.data_ptr()
+            a.lr, a.beta1, a.beta2, a.eps, a.momentum, a.t = lr, 0.9, 0.999, 1e-8, 0.9, t + 1
+            a.shadow_bf16, a.n_shadow, a.nonfinite = None, 0, bad.data_ptr()
+            _lib.check(_lib.lib().moep_optim_step(a, torch.cuda.current_stream().cuda_stream), "optim")
+        want = np.concatenate([g[f"{opt}_p3_w"].ravel(), g[f"{opt}_p3_b"]])
+        assert np.allclose(p.cpu().numpy(), want, rtol=1e-14, atol=1e-15), opt
+
+
+def _dataset(O, n=1200, d=16, e=8, k=2, seed=7):
+    r = np.random.default_rng(seed)
+    gate = r.standard_normal((e, d)) / 4.0
+    x = r.standard_normal((n, d))
+    scores = O.teacher_scores(x, gate).astype(np.float32)
+    acts = x.astype(np.float32)
+    topk = O.top_k_batch(scores.astype(np.float64), k)
+    return acts, scores, topk
+
+
+@pytest.mark.parametrize("family", ["wbce", "ranking", "focal", "mse"])
+def test_train_fp64_matches_oracle_loop(pb, O, family):
+    acts, scores, topk = _dataset(O)
+    cfg = pb.TrainConfig(loss=pb.LossSpec(family=family), hidden=32, batch_size=64, epochs=2, seed=5,
+                         eval_fraction=0.2, precision="fp64")
+    data = pb.TraceFile(16, 8, 2, acts, scores, topk)
+    model, report = pb.train(cfg, data)
+    p, rows, _ = O.train_arch2(acts, scores, topk, 2, hidden=32, batch_size=64, epochs=2, seed=5,
+                               eval_fraction=0.2, loss={"family": family})
+    for name in ("w1", "b1", "w2", "b2"):
+        assert np.allclose(getattr(model, name), p[name], rtol=1e-8, atol=1e-10), name
+    for ours, ref in zip(report.epochs, rows):
+        assert ours.train_loss == pytest.approx(ref[0], rel=1e-9)
+        assert (ours.exact_match, ours.top1, ours.overprov) == pytest.approx(ref[1:], abs=0)
+
+
+def test_train_c4_shape_fp32_step_within_tolerance(pb, O):
+    """Phi-mini shape (d=4096, h=2048, E=16, k=2), arch2 + ranking, one fp32 tensor-core
+    step vs the fp64 oracle step: loss rel 1e-3, parameter update rel 2e-2."""
+    r = np.random.default_rng(1)
+    n, d, h, e, k = 256, 4096, 2048, 16, 2
+    m = pb.init_model("arch2", d, h, e, seed=3)
+    m.w1, m.w2 = O.round_bf16(m.w1), O.round_bf16(m.w2)
+    x = O.round_bf16(r.standard_normal((n, d)))
+    scores = O.teacher_scores(x, r.standard_normal((e, d)) / 64.0)
+    spec = pb.LossSpec(family="ranking")
+    tr = pb.DeviceTrainer(m, spec, "adam", 1e-3, precision="fp32")
+    lab = pb.BatchLabels.from_scores(torch.as_tensor(scores).cuda(), k)
+    out = tr.step(torch.as_tensor(x).cuda().to(torch.bfloat16), lab.true_scores.float().contiguous(),
+                  lab.topk_mask.to(torch.uint8).contiguous(), lab.rank_of.contiguous())
+    p = {"arch": "arch2", "w1": m.w1.copy(), "b1": m.b1.copy(), "w2": m.w2.copy(), "b2": m.b2.copy()}
+    z, cache = O.forward_eval(p, x)
+    olab = O.batch_labels(scores, k)
+    lv, dz = O.loss_and_grad({"family": "ranking"}, z, olab)
+    g = O.backward_eval(p, cache, dz)
+    assert float(out[0].item()) == pytest.approx(lv, rel=1e-3)
+    gw1 = tr.view(tr.grad, 0).double().cpu().numpy()
+    assert np.linalg.norm(gw1 - g["w1"]) / np.linalg.norm(g["w1"]) < 2e-2
+    gw2 = tr.view(tr.grad, 1).double().cpu().numpy()
+    assert np.linalg.norm(gw2 - g["w2"]) / np.linalg.norm(g["w2"]) < 2e-2
