@@ -33,6 +33,20 @@ __device__ __forceinline__ double ld(const void* p, int64_t i) {
   return reinterpret_cast<const double*>(p)[i];
 }
 
+// Exact bf16 -> fp64 with integer ops (the F2F.F64.F32 conversion path is a
+// low-throughput pipe and dominated the inner loop). u holds the 16-bit
+// pattern in its low half. Zero is handled inline; bf16 subnormals, inf and
+// NaN (t outside [0x80, 0x7f80)) take the exact slow path.
+__device__ __forceinline__ double bf16_to_f64(uint32_t u) {
+  const uint32_t t = u & 0x7fffu;
+  uint32_t hi = (t << 13) + 0x38000000u;  // exponent rebias 127 -> 1023
+  hi = (t == 0u) ? 0u : hi;
+  hi |= (u & 0x8000u) << 16;
+  double r = __hiloint2double(static_cast<int>(hi), 0);
+  if (t != 0u && (t - 0x80u) >= 0x7f00u) r = static_cast<double>(__uint_as_float(u << 16));
+  return r;
+}
+
 // 8 consecutive weights starting at element i (i % 8 == 0) as doubles
 template <int T>
 __device__ __forceinline__ void ld8(const void* p, int64_t i, double* w) {
@@ -41,8 +55,8 @@ __device__ __forceinline__ void ld8(const void* p, int64_t i, double* w) {
     const uint32_t q[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      w[2 * c] = static_cast<double>(__uint_as_float(q[c] << 16));
-      w[2 * c + 1] = static_cast<double>(__uint_as_float(q[c] & 0xffff0000u));
+      w[2 * c] = bf16_to_f64(q[c] & 0xffffu);
+      w[2 * c + 1] = bf16_to_f64(q[c] >> 16);
     }
   } else {
     const double2* d2 = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(p) + i);
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(NT, 1) fp64_kernel(moep_fp64_args a, int n_cou
 
 template <int XT, int WT, int TB>
 size_t smem_bytes(int d, int E) {
-  using XS = typename std::conditional<XT == MOEP_BF16, float, double>::type;
+  using XS = double;  // staged once per group; avoids per-use conversions
   const int dpad = (d + IV - 1) / IV * IV;
   return sizeof(double) * (TB * HP + TB * E) + sizeof(XS) * static_cast<size_t>(dpad) * TB +
          sizeof(int) * (TB * E + 2 * E);
@@ -263,7 +277,7 @@ size_t smem_bytes(int d, int E) {
 
 template <int XT, int WT, int TB>
 int launch(const moep_fp64_args* a, cudaStream_t st, int ncnt) {
-  using XS = typename std::conditional<XT == MOEP_BF16, float, double>::type;
+  using XS = double;
   const size_t smem = smem_bytes<XT, WT, TB>(a->d, a->n_experts);
   auto kern = fp64_kernel<XT, WT, TB, XS>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
