@@ -1,0 +1,228 @@
+// k1_common.cuh — parameters and the per-token selection / evaluation epilogue
+// shared by the fused predictor kernels.
+#pragma once
+#include <cstdint>
+#include "sm100.cuh"
+#include "common.cuh"
+
+namespace moep {
+namespace k1c {
+
+struct Params {
+  int64_t n_tokens;
+  int d, hidden, E, arch;
+  const float* b1;
+  const float* alpha;
+  const float* beta;
+  const float* b2;
+  int m_sel, n_bounds;
+  int bounds[MOEP_MAX_BOUNDS];
+  float tau_abs, tau_rel, w2_norm;
+  int* ids;
+  float* logits;
+  uint8_t* flags;
+  int* flag_list;
+  int* flag_count;
+  const int* truth;
+  int k, n_m;
+  int m_list[MOEP_MAX_BOUNDS];
+  int* partials;
+  int n_counters;
+  float* a_out;
+};
+
+// mbarrier wait that traps instead of hanging forever (a lost arrival becomes a
+// launch error, not a wedged GPU).
+__device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0, spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (++spins == (1u << 26)) {
+      printf("moep k1: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+      asm volatile("trap;");
+    }
+  }
+}
+
+// z[EP]: this token's raw GEMM2 accumulator (no b2). Every lane of the warp
+// must call this (ballots). Mirrors predict_topk_batch / top_k_batch
+// (predictor.py:347-351, core.py:42-48) and metrics.py:159-180.
+template <int EP>
+__device__ __forceinline__ void row_epilogue(const Params& p, float* z, float sumsq, int64_t row, bool valid,
+                                             uint32_t lane, int* hist, RowCounters& rc) {
+  bool flagged = false;
+#pragma unroll
+  for (int e = 0; e < EP; ++e) {
+    if (e < p.E) {
+      z[e] += __ldg(p.b2 + e);
+      flagged |= !isfinite(z[e]);
+    } else {
+      z[e] = -INFINITY;
+    }
+  }
+  int P = p.m_sel;
+#pragma unroll
+  for (int b = 0; b < MOEP_MAX_BOUNDS; ++b)
+    if (b < p.n_bounds && p.bounds[b] > P) P = p.bounds[b];
+  P = min(P + 1, min(p.E, kMaxSel));
+  float tv[kMaxSel];
+  int tix[kMaxSel];
+  {
+    uint32_t taken[(EP + 31) / 32];
+#pragma unroll
+    for (int w = 0; w < (EP + 31) / 32; ++w) taken[w] = 0;
+#pragma unroll
+    for (int s = 0; s < kMaxSel; ++s) {
+      float best = -INFINITY;
+      int bi = 0;
+      if (s < P) {
+#pragma unroll
+        for (int e = 0; e < EP; ++e) {
+          const bool tk = (taken[e >> 5] >> (e & 31)) & 1u;
+          if (!tk && z[e] > best) { best = z[e]; bi = e; }
+        }
+#pragma unroll
+        for (int w = 0; w < (EP + 31) / 32; ++w)
+          if ((bi >> 5) == w) taken[w] |= 1u << (bi & 31);
+      }
+      tv[s] = best;
+      tix[s] = bi;
+    }
+  }
+  const float delta = p.tau_abs + p.tau_rel * sqrtf(sumsq) * p.w2_norm;
+#pragma unroll
+  for (int b = 0; b < MOEP_MAX_BOUNDS; ++b) {
+    if (b < p.n_bounds) {
+      const int pos = p.bounds[b];
+      if (pos >= 1 && pos < p.E) {
+        float hi_v = tv[0], lo_v = tv[1];
+#pragma unroll
+        for (int s = 1; s < kMaxSel; ++s)
+          if (s == pos) { hi_v = tv[s - 1]; lo_v = tv[s]; }
+        flagged |= !(hi_v - lo_v >= delta);
+      }
+    }
+  }
+  if (valid) {
+    if (p.flags) p.flags[row] = flagged ? 1 : 0;
+    if (flagged) {
+      const int slot = atomicAdd(p.flag_count, 1);
+      p.flag_list[slot] = static_cast<int>(row);
+    }
+    if (p.logits) {
+      float* lrow = p.logits + row * p.E;
+#pragma unroll
+      for (int e = 0; e < EP; ++e)
+        if (e < p.E) lrow[e] = z[e];
+    }
+    if (p.ids && !flagged) {
+      int* orow = p.ids + row * p.m_sel;
+      if (p.m_sel >= p.E) {
+        for (int e = 0; e < p.E; ++e) orow[e] = e;
+      } else {
+        float thv = tv[0];
+        int thi = tix[0];
+#pragma unroll
+        for (int s = 0; s < kMaxSel; ++s)
+          if (s == p.m_sel - 1) { thv = tv[s]; thi = tix[s]; }
+        int cnt = 0;
+#pragma unroll
+        for (int e = 0; e < EP; ++e)
+          if (e < p.E && (key_gt(z[e], e, thv, thi) || e == thi)) orow[cnt++] = e;
+      }
+    }
+  }
+  if (p.truth) {
+    const bool use = valid && !flagged;
+    int tr[16], te[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      tr[j] = 0;
+      te[j] = -1;
+      if (use && j < p.k) {
+        const int t = __ldg(p.truth + row * p.k + j);
+        te[j] = t;
+        float zt = 0.f;
+#pragma unroll
+        for (int e = 0; e < EP; ++e)
+          if (e == t) zt = z[e];
+        int r = 0;
+#pragma unroll
+        for (int e = 0; e < EP; ++e) r += (e < p.E && key_gt(z[e], e, zt, t)) ? 1 : 0;
+        tr[j] = r;
+      }
+    }
+    if (use) {
+      rc.n += 1;
+      bool any0 = false;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) any0 |= (j < p.k && tr[j] == 0);
+      rc.top1 += any0 ? 1 : 0;
+#pragma unroll
+      for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
+        if (mi < p.n_m) {
+          const int m = p.m_list[mi];
+          int inside = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) inside += (j < p.k && tr[j] < m) ? 1 : 0;
+          rc.ov[mi] += (inside == p.k) ? 1 : 0;
+          rc.rc[mi] += inside;
+        }
+      }
+    }
+    for (int e = 0; e < p.E; ++e) {
+      bool has = false, hit = false;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < p.k && te[j] == e) { has = true; hit = tr[j] < p.k; }
+      const uint32_t bt = __ballot_sync(0xffffffffu, has);
+      const uint32_t bh = __ballot_sync(0xffffffffu, hit);
+      if (lane == (e & 31)) {
+        hist[e] += __popc(bh);
+        hist[EP + e] += __popc(bt);
+      }
+    }
+  }
+}
+
+// Per-CTA partial counters from the 4 warps of the selecting warpgroup
+// (named barrier `bar_id`, 128 threads). red: int[4][16] smem, hist0: int[4][2][EP].
+template <int EP>
+__device__ __forceinline__ void write_partials(const Params& p, const RowCounters& rc, int q, uint32_t lane,
+                                               int tid_in_wg, int* red0, int* hist0, int bar_id) {
+  int* red = red0 + q * 16;
+  const int vals[2 + 2 * MOEP_MAX_BOUNDS] = {rc.n, rc.top1, rc.ov[0], rc.ov[1], rc.ov[2],
+                                              rc.ov[3], rc.rc[0], rc.rc[1], rc.rc[2], rc.rc[3]};
+#pragma unroll
+  for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) {
+    const int s = warp_sum(vals[i]);
+    if (lane == 0) red[i] = s;
+  }
+  asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+  int* out = p.partials + static_cast<int64_t>(blockIdx.x) * p.n_counters;
+  const int t = tid_in_wg;
+  if (t < 2 + 2 * p.n_m) {
+    const int src = t < 2 ? t : (t < 2 + p.n_m ? 2 + (t - 2) : 2 + MOEP_MAX_BOUNDS + (t - 2 - p.n_m));
+    out[t] = red0[src] + red0[16 + src] + red0[32 + src] + red0[48 + src];
+  }
+  const int base = 2 + 2 * p.n_m;
+  for (int e = t; e < p.E; e += 128) {
+    int hsum = 0, tsum = 0;
+    for (int w = 0; w < 4; ++w) {
+      hsum += hist0[w * 2 * EP + e];
+      tsum += hist0[w * 2 * EP + EP + e];
+    }
+    out[base + e] = hsum;
+    out[base + p.E + e] = tsum;
+  }
+}
+
+}  // namespace k1c
+}  // namespace moep

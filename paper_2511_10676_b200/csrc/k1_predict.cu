@@ -20,6 +20,7 @@
 // runs on hi and lo halves of the hidden so the hidden loses < 2^-17 relative;
 // any token whose decision gap is below tau is flagged for the fp64 kernel K2.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include "sm100.cuh"
 #include "common.cuh"
@@ -525,6 +526,8 @@ int launch_k1(const moep_predict_args* a, cudaStream_t st, const CUtensorMap& tx
 }
 }  // namespace
 
+extern "C" int moep_predict_bf16_pair(const moep_predict_args* a, void* stream);
+
 extern "C" int moep_predict_bf16(const moep_predict_args* a, void* stream) {
   using namespace moep::k1;
   if (!a || a->n_tokens <= 0 || a->d <= 0 || a->hidden <= 0 || a->n_experts <= 0) return MOEP_ESHAPE;
@@ -539,6 +542,14 @@ extern "C" int moep_predict_bf16(const moep_predict_args* a, void* stream) {
   if (!a->flag_list || !a->flag_count) return MOEP_EARG;
   if (a->arch == 2 && !a->b1) return MOEP_EARG;
   if (a->arch == 1 && (!a->act_alpha || !a->act_beta)) return MOEP_EARG;
+  // The CTA-pair kernel (k1v2_predict.cu) covers hidden % 256 == 0; the 1-SM
+  // kernel below handles every other shape. MOEP_K1_VARIANT=1 forces the latter.
+  static int variant = -1;
+  if (variant < 0) {
+    const char* env = getenv("MOEP_K1_VARIANT");
+    variant = (env && env[0] == '1') ? 1 : 2;
+  }
+  if (variant == 2 && a->hidden % 256 == 0) return moep_predict_bf16_pair(a, stream);
   int EP = 16;
   while (EP < a->n_experts) EP *= 2;
   CUtensorMap tx, tw1, tw2;

@@ -1,0 +1,374 @@
+// k1v2_predict.cu — K1 v2: fused expert predictor on a CTA pair (cta_group::2).
+//
+// Same math and outputs as k1_predict.cu (reference: predictor.py:193-240,
+// :330-351; core.py:27-48; metrics.py:138-193), re-tiled for the Blackwell
+// 2-SM tensor core:
+//   * a cluster of 2 CTAs owns a 256-token tile; one tcgen05.mma.cta_group::2
+//     (M=256, N=256, K=16) covers 256 tokens x 256 hidden units, each CTA
+//     staging its own 128 x-rows and half of the W1 chunk (128 rows) -> per-SM
+//     shared-memory traffic per MAC is half of the 1-SM 128x128 tile, and x is
+//     re-streamed h/256 instead of h/128 times;
+//   * GEMM1 accumulates a 256-column chunk in TMEM (single buffer); the epilogue
+//     drains it into registers at once (setmaxnreg gives the epilogue 224 regs)
+//     so the next chunk's MMAs start after a short drain;
+//   * bias + activation + bf16 hi/lo split go to a 64 KB smem A operand, fed to
+//     GEMM2 (M=256, N=E) in two K-halves so one buffer suffices;
+//   * the per-token selection / margin flag / evaluation epilogue is shared
+//     with K1 v1 (k1_common.cuh).
+// Warp roles (per CTA, 12 warps): 0 TMA x+W1, 1 MMA issue (leader CTA only),
+// 2 TMA W2, 3 TMEM alloc, 4-11 epilogue (WG0 = columns 0-127 of the chunk and
+// the token epilogue, WG1 = columns 128-255).
+// Requires hidden % 256 == 0 and E <= 128 (else the 1-SM kernel is used).
+#include <cstdio>
+#include <cuda.h>
+#include "sm100.cuh"
+#include "common.cuh"
+#include "k1_common.cuh"
+#include "tmap.cuh"
+
+namespace moep {
+namespace k1v2 {
+
+using k1c::Params;
+using k1c::wait;
+
+constexpr int BM = 128;         // tokens per CTA (256 per pair)
+constexpr int BK = 64;          // K per stage
+constexpr int HC = 256;         // hidden columns per chunk (pair MMA N)
+constexpr int HB = HC / 2;      // W1 rows staged per CTA
+constexpr int NTHREADS = 384;
+constexpr int EPI_WARP0 = 4;
+
+template <int EP>
+struct Cfg {
+  static constexpr int STAGES = (EP <= 64) ? 4 : 3;
+  static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
+  static constexpr int B_BYTES = HB * BK * 2;        // 16 KB
+  static constexpr int ATOM = BM * 64 * 2;           // 16 KB: 128 rows x 64 bf16 (SW128)
+  static constexpr int W2_ROWS = EP / 2;             // expert rows staged per CTA
+  static constexpr int W2_ATOM = W2_ROWS * 128;      // bytes per 64-column atom
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
+  static constexpr int OFF_A2 = OFF_B + STAGES * B_BYTES;  // [hi atom0, hi atom1, lo atom0, lo atom1]
+  static constexpr int OFF_W2 = OFF_A2 + 4 * ATOM;          // 4 atoms (256 columns)
+  static constexpr int OFF_HIST = OFF_W2 + ((4 * W2_ATOM + 1023) / 1024) * 1024;
+  static constexpr int OFF_SUMSQ = OFF_HIST + 4 * 2 * EP * 4;
+  static constexpr int OFF_RED = OFF_SUMSQ + BM * 4;
+  static constexpr int OFF_BAR = OFF_RED + 4 * 16 * 4;
+  static constexpr int NBAR = 2 * STAGES + 10;
+  static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
+  static constexpr uint32_t ZCOL = HC;  // TMEM column of the z accumulator
+};
+
+template <int EP, int ARCH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w1,
+                    const __grid_constant__ CUtensorMap tm_w2, const Params p) {
+  using C = Cfg<EP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* full = bars;                      // [STAGES] leader: x+W1 of both CTAs landed
+  uint64_t* empty = bars + C::STAGES;         // [STAGES] local: stage consumed (multicast commit)
+  uint64_t* acc_full = empty + C::STAGES;     // local: GEMM1 chunk done
+  uint64_t* acc_empty = acc_full + 1;         // leader: 16 epilogue warps drained
+  uint64_t* a2_full = acc_empty + 1;          // [2] leader: 8 warps wrote that K-half of A2
+  uint64_t* a2_emptyA = a2_full + 2;          // local: GEMM2 half 0 consumed A2
+  uint64_t* a2_emptyB = a2_emptyA + 1;        // local: GEMM2 half 1 consumed A2
+  uint64_t* w2_full = a2_emptyB + 1;          // leader: W2 chunk of both CTAs landed
+  uint64_t* w2_empty = w2_full + 1;           // local
+  uint64_t* z_full = w2_empty + 1;            // local
+  uint64_t* z_empty = z_full + 1;             // leader: 8 warps read z
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int num_tiles = static_cast<int>((p.n_tokens + 2 * BM - 1) / (2 * BM));
+  const int nchunks = p.hidden / HC;
+  const int nk = (p.d + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 16);
+    mbar_init(&a2_full[0], 8);
+    mbar_init(&a2_full[1], 8);
+    mbar_init(a2_emptyA, 1);
+    mbar_init(a2_emptyB, 1);
+    mbar_init(w2_full, 1);
+    mbar_init(w2_empty, 1);
+    mbar_init(z_full, 1);
+    mbar_init(z_empty, 8);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_x); tma_prefetch_desc(&tm_w1); tma_prefetch_desc(&tm_w2);
+  }
+  if (warp == 3) tmem_alloc_cg2<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < EPI_WARP0) {
+    if (warp == 0) {
+      // ---------------------------------------------- TMA: x rows + W1 half-chunk
+      if (elect_one()) {
+        const uint64_t keep = policy_evict_last();
+        uint32_t stage = 0, phase = 0;
+        for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+          const int xrow = tile * 2 * BM + rank * BM;
+          for (int c = 0; c < nchunks; ++c) {
+            const int wrow = c * HC + rank * HB;
+            for (int kb = 0; kb < nk; ++kb) {
+              wait(&empty[stage], phase ^ 1);
+              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+              tma_load_2d_cg2(&tm_x, &full[stage], smem + C::OFF_A + stage * C::A_BYTES, kb * BK, xrow, keep);
+              tma_load_2d_cg2(&tm_w1, &full[stage], smem + C::OFF_B + stage * C::B_BYTES, kb * BK, wrow, keep);
+              if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+        }
+      }
+    } else if (warp == 2) {
+      // ---------------------------------------------- TMA: W2 chunk (EP/2 rows per CTA)
+      if (elect_one()) {
+        const uint64_t keep = policy_evict_last();
+        uint32_t n = 0;
+        for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+          for (int c = 0; c < nchunks; ++c, ++n) {
+            if (n > 0) wait(w2_empty, (n - 1) & 1);
+            if (leader) mbar_arrive_expect_tx(w2_full, 2 * 4 * C::W2_ATOM);
+#pragma unroll
+            for (int at = 0; at < 4; ++at)
+              tma_load_2d_cg2(&tm_w2, w2_full, smem + C::OFF_W2 + at * C::W2_ATOM, c * HC + at * 64,
+                              rank * C::W2_ROWS, keep);
+          }
+        }
+      }
+    } else if (warp == 1 && leader) {
+      // ---------------------------------------------- MMA issuer (pair leader)
+      if (elect_one()) {
+        const uint32_t idesc1 = idesc_bf16_f32(2 * BM, HC);
+        const uint32_t idesc2 = idesc_bf16_f32(2 * BM, EP);
+        const uint32_t a_base = smem_u32(smem + C::OFF_A), b_base = smem_u32(smem + C::OFF_B);
+        const uint32_t a2_base = smem_u32(smem + C::OFF_A2), w2_base = smem_u32(smem + C::OFF_W2);
+        uint32_t stage = 0, phase = 0, gc = 0, ti = 0;
+        auto gemm2 = [&](int cc, uint32_t chunk_id) {
+          if (cc == 0) wait(z_empty, (ti & 1) ^ 1);
+          wait(w2_full, chunk_id & 1);
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            wait(&a2_full[half], chunk_id & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const int at = kk >> 2, w = kk & 3;
+              const uint64_t bd = sdesc_k_sw128(w2_base + (half * 2 + at) * C::W2_ATOM + w * 32);
+              const uint64_t ahi = sdesc_k_sw128(a2_base + at * C::ATOM + w * 32);
+              const uint64_t alo = sdesc_k_sw128(a2_base + (2 + at) * C::ATOM + w * 32);
+              umma_bf16_cg2(tmem + C::ZCOL, ahi, bd, idesc2, (cc | half | kk) != 0);
+              umma_bf16_cg2(tmem + C::ZCOL, alo, bd, idesc2, 1u);
+            }
+            umma_commit_mc(half == 0 ? a2_emptyA : a2_emptyB, 0x3);
+          }
+          umma_commit_mc(w2_empty, 0x3);
+          if (cc == nchunks - 1) umma_commit_mc(z_full, 0x3);
+        };
+        for (int tile = pair; tile < num_tiles; tile += n_pairs, ++ti) {
+          for (int c = 0; c < nchunks; ++c, ++gc) {
+            wait(acc_empty, (gc & 1) ^ 1);
+            tc_fence_after();
+            for (int kb = 0; kb < nk; ++kb) {
+              wait(&full[stage], phase);
+              tc_fence_after();
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k) {
+                const uint64_t ad = sdesc_k_sw128(a_base + stage * C::A_BYTES + k * 32);
+                const uint64_t bd = sdesc_k_sw128(b_base + stage * C::B_BYTES + k * 32);
+                umma_bf16_cg2(tmem, ad, bd, idesc1, (kb | k) != 0);
+              }
+              umma_commit_mc(&empty[stage], 0x3);
+              if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            }
+            umma_commit_mc(acc_full, 0x3);
+            if (c > 0) gemm2(c - 1, gc - 1);
+          }
+          gemm2(nchunks - 1, gc - 1);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue warpgroups
+    const int wg = (warp - EPI_WARP0) >> 2;  // 0: chunk columns 0-127, 1: 128-255
+    const uint32_t q = warp & 3;
+    const int row_in_tile = q * 32 + lane;
+    const uint32_t lane_addr = (q * 32) << 16;
+    float* s_sumsq = reinterpret_cast<float*>(smem + C::OFF_SUMSQ);
+    int* hist0 = reinterpret_cast<int*>(smem + C::OFF_HIST);
+    int* hist = hist0 + q * 2 * EP;
+    if (wg == 0)
+      for (int e = lane; e < 2 * EP; e += 32) hist[e] = 0;
+    RowCounters rc;
+    rc.zero();
+    uint32_t gc = 0, ti = 0;
+    for (int tile = pair; tile < num_tiles; tile += n_pairs, ++ti) {
+      const int64_t row_g = static_cast<int64_t>(tile) * 2 * BM + rank * BM + row_in_tile;
+      float sumsq = 0.f;
+      for (int c = 0; c < nchunks; ++c, ++gc) {
+        wait(acc_full, gc & 1);
+        tc_fence_after();
+        float v[128];
+        const uint32_t ta = tmem + lane_addr + wg * 128;
+        tmem_ld32(ta, v);
+        tmem_ld32(ta + 32, v + 32);
+        tmem_ld32(ta + 64, v + 64);
+        tmem_ld32(ta + 96, v + 96);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(acc_empty, 0);
+        // bias + activation + hi/lo split, in place per column pair (2j, 2j+1):
+        // v[2j] <- packed bf16x2 hi, v[2j+1] <- packed bf16x2 lo
+        const int col0 = c * HC + wg * 128;
+#pragma unroll
+        for (int j4 = 0; j4 < 32; ++j4) {
+          const int col = col0 + j4 * 4;
+          float hv[4];
+          if (ARCH == 2) {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(p.b1 + col));
+            const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+            if (p.a_out && row_g < p.n_tokens)
+              *reinterpret_cast<float4*>(p.a_out + row_g * p.hidden + col) =
+                  make_float4(v[j4 * 4] + bv[0], v[j4 * 4 + 1] + bv[1], v[j4 * 4 + 2] + bv[2], v[j4 * 4 + 3] + bv[3]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) hv[t] = silu_f32(v[j4 * 4 + t] + bv[t]);
+          } else {
+            const float4 aa = __ldg(reinterpret_cast<const float4*>(p.alpha + col));
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(p.beta + col));
+            const float av[4] = {aa.x, aa.y, aa.z, aa.w}, bv[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) hv[t] = gelu_tanh_f32(fmaf(av[t], v[j4 * 4 + t], bv[t]));
+          }
+#pragma unroll
+          for (int t = 0; t < 4; t += 2) {
+            sumsq = fmaf(hv[t], hv[t], sumsq);
+            sumsq = fmaf(hv[t + 1], hv[t + 1], sumsq);
+            const __nv_bfloat16 h0 = __float2bfloat16_rn(hv[t]);
+            const __nv_bfloat16 h1 = __float2bfloat16_rn(hv[t + 1]);
+            const __nv_bfloat16 l0 = __float2bfloat16_rn(hv[t] - __bfloat162float(h0));
+            const __nv_bfloat16 l1 = __float2bfloat16_rn(hv[t + 1] - __bfloat162float(h1));
+            v[j4 * 4 + t] = __uint_as_float(static_cast<uint32_t>(__bfloat16_as_ushort(h0)) |
+                                            (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16));
+            v[j4 * 4 + t + 1] = __uint_as_float(static_cast<uint32_t>(__bfloat16_as_ushort(l0)) |
+                                                (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16));
+          }
+        }
+        // the A2 buffer is free once the previous GEMM2 half that read it completed
+        if (wg == 0) {
+          if (gc > 0) wait(a2_emptyB, (gc - 1) & 1);
+        } else {
+          wait(a2_emptyA, gc & 1);
+        }
+        uint8_t* a2hi = smem + C::OFF_A2;
+        uint8_t* a2lo = smem + C::OFF_A2 + 2 * C::ATOM;
+#pragma unroll
+        for (int sb = 0; sb < 4; ++sb) {
+          const int at = sb >> 1;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            // 16-byte chunk = 8 columns = 4 column pairs starting at column sb*32 + ch*8
+            const uint32_t off = at * C::ATOM + sw128_offset(row_in_tile, (sb & 1) * 32 + ch * 8);
+            const int b = sb * 32 + ch * 8;
+            *reinterpret_cast<uint4*>(a2hi + off) = make_uint4(__float_as_uint(v[b]), __float_as_uint(v[b + 2]),
+                                                               __float_as_uint(v[b + 4]), __float_as_uint(v[b + 6]));
+            *reinterpret_cast<uint4*>(a2lo + off) = make_uint4(__float_as_uint(v[b + 1]), __float_as_uint(v[b + 3]),
+                                                               __float_as_uint(v[b + 5]), __float_as_uint(v[b + 7]));
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&a2_full[wg], 0);
+      }
+      // ---- token epilogue on warpgroup 0
+      if (wg == 1) s_sumsq[row_in_tile] = sumsq;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (wg == 0) {
+        sumsq += s_sumsq[row_in_tile];
+        wait(z_full, ti & 1);
+        tc_fence_after();
+        float z[EP];
+#pragma unroll
+        for (int j = 0; j < EP; j += 16) tmem_ld16(tmem + lane_addr + C::ZCOL + j, z + j);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(z_empty, 0);
+        k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc);
+      }
+    }
+    if (wg == 0 && p.partials)
+      k1c::write_partials<EP>(p, rc, q, lane, threadIdx.x - EPI_WARP0 * 32,
+                              reinterpret_cast<int*>(smem + C::OFF_RED), hist0, 2);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 3) tmem_dealloc_cg2<512>(tmem);
+}
+
+}  // namespace k1v2
+}  // namespace moep
+
+namespace {
+template <int EP, int ARCH>
+int launch_v2(const moep_predict_args* a, cudaStream_t st) {
+  using namespace moep::k1v2;
+  using C = Cfg<EP>;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto kern = predict_pair_kernel<EP, ARCH>;
+  if (!attr_set[dev]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
+      return MOEP_ELAUNCH;
+    attr_set[dev] = true;
+  }
+  CUtensorMap tx, tw1, tw2;
+  if (moep::make_tmap_bf16(&tx, a->x, a->n_tokens, a->d, BM, BK) ||
+      moep::make_tmap_bf16(&tw1, a->w1, a->hidden, a->d, HB, BK) ||
+      moep::make_tmap_bf16(&tw2, a->w2, a->n_experts, a->hidden, C::W2_ROWS, 64))
+    return MOEP_EALIGN;
+  moep::k1c::Params p{};
+  p.n_tokens = a->n_tokens; p.d = a->d; p.hidden = a->hidden; p.E = a->n_experts; p.arch = a->arch;
+  p.b1 = a->b1; p.alpha = a->act_alpha; p.beta = a->act_beta; p.b2 = a->b2;
+  p.m_sel = a->m_sel; p.n_bounds = a->n_bounds;
+  for (int i = 0; i < MOEP_MAX_BOUNDS; ++i) { p.bounds[i] = a->bounds[i]; p.m_list[i] = a->m_list[i]; }
+  p.tau_abs = a->tau_abs; p.tau_rel = a->tau_rel; p.w2_norm = a->w2_norm;
+  p.ids = a->ids; p.logits = a->logits; p.flags = a->flags;
+  p.flag_list = a->flag_list; p.flag_count = a->flag_count;
+  p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;
+  p.n_counters = moep_n_counters(a->n_m, a->n_experts);
+  const int grid = moep_num_sms() & ~1;  // whole CTA pairs
+  kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+}  // namespace
+
+// Pair kernel entry (validation shared with moep_predict_bf16, which dispatches here).
+extern "C" int moep_predict_bf16_pair(const moep_predict_args* a, void* stream) {
+  if (a->hidden % 256 != 0 || a->n_experts > 128) return MOEP_EUNSUPPORTED;
+  int EP = 16;
+  while (EP < a->n_experts) EP *= 2;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool a1 = a->arch == 1;
+  switch (EP) {
+    case 16: return a1 ? launch_v2<16, 1>(a, st) : launch_v2<16, 2>(a, st);
+    case 32: return a1 ? launch_v2<32, 1>(a, st) : launch_v2<32, 2>(a, st);
+    case 64: return a1 ? launch_v2<64, 1>(a, st) : launch_v2<64, 2>(a, st);
+    default: return a1 ? launch_v2<128, 1>(a, st) : launch_v2<128, 2>(a, st);
+  }
+}
