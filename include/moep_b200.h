@@ -111,9 +111,18 @@ typedef struct {
   const int32_t* truth; int32_t k; int32_t n_m; int32_t m_list[MOEP_MAX_BOUNDS];
   int32_t* partials;          /* [moep_num_sms(), n_counters] */
   double* a_out;              /* [N, hidden] fp64 pre-activation (training, exact mode), or NULL */
+  int64_t row_begin;          /* first list index handled (rows mode) / first row (all rows) */
 } moep_fp64_args;
 
 int moep_predict_fp64(const moep_fp64_args* a, void* stream);
+
+/* K2 fast path for the flagged rows: register-blocked fp64 GEMM over the rows
+ * in rows[0 .. min(*row_count, capacity)) with per-hidden-tile partial logits
+ * in `scratch` (capacity * ceil(hidden/128) * E doubles), then a per-token
+ * finish kernel; rows beyond the capacity go through moep_predict_fp64 with
+ * their evaluation partials in partials2 ([moep_num_sms(), n_counters]). */
+int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t capacity, int32_t* partials2,
+                    void* stream);
 
 /* ------------------------------------------------------------------ K7 --
  * Evaluation / selection from given logits (fp64 or fp32), exact compares.

@@ -44,7 +44,7 @@ class Fp64Args(C.Structure):
         ("bn_var", vp), ("bn_eps", f64), ("w2", vp), ("w2t", vp), ("b2", vp),
         ("rows", vp), ("row_count", vp), ("m_sel", i32), ("ids", vp), ("logits64", vp), ("logits32", vp),
         ("truth", vp), ("k", i32), ("n_m", i32), ("m_list", i32 * MAX_BOUNDS), ("partials", vp),
-        ("a_out", vp),
+        ("a_out", vp), ("row_begin", i64),
     ]
 
 
@@ -71,6 +71,7 @@ class OptimArgs(C.Structure):
 _SIGS = {
     "moep_predict_bf16": [C.POINTER(PredictArgs), vp],
     "moep_predict_fp64": [C.POINTER(Fp64Args), vp],
+    "moep_fixup_fp64": [C.POINTER(Fp64Args), vp, i64, vp, vp],
     "moep_eval_logits": [vp, i32, i64, i32, vp, i32, i32, vp, vp, vp],
     "moep_topk_logits": [vp, i32, i64, i32, i32, vp, vp],
     "moep_rank_order": [vp, i32, i64, i32, vp, vp],

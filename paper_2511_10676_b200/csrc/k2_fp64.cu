@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(NT, 1) fp64_kernel(moep_fp64_args a, int n_cou
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < 2 * E; i += NT) hist[i] = 0;
   if (tid < 2 + 2 * MOEP_MAX_BOUNDS) scal[tid] = 0;
-  const int64_t nrows = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
+  const int64_t nall = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
+  const int64_t nrows = nall > a.row_begin ? nall - a.row_begin : 0;  // rows handled here
   const int64_t ngroups = (nrows + TB - 1) / TB;
   const bool vec_ok = (d % IV) == 0;
   __syncthreads();
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(NT, 1) fp64_kernel(moep_fp64_args a, int n_cou
     const int64_t left = nrows - g * TB;
     const int nt = left < TB ? static_cast<int>(left) : TB;
     if (tid < TB) {
-      const int64_t it = g * TB + tid;
+      const int64_t it = a.row_begin + g * TB + tid;
       rowid[tid] = tid < nt ? (a.rows ? a.rows[it] : it) : -1;
     }
     __syncthreads();

@@ -224,6 +224,18 @@ class DevicePredictor:
                 and self.d % 8 == 0 and self.hidden % 8 == 0
                 and all(p <= K1_MAX_SEL or p >= self.E for p in positions))
 
+    fixup_capacity = None  # rows handled by the GEMM fix-up per call (None: max(2048, N/128))
+
+    def _fixup(self, a, n, partials2=None):
+        """Exact fp64 recompute of K1's flagged rows (fast GEMM path + overflow)."""
+        cap = self.fixup_capacity or max(2048, n // 128)
+        if cap > n:
+            cap = n
+        ntile_h = (self.hidden + 127) // 128
+        scratch = torch.empty(cap * ntile_h * self.E, dtype=torch.float64, device=self.device)
+        check(lib().moep_fixup_fp64(a, ptr(scratch), cap, ptr(partials2), _stream(self.device)),
+              "moep_fixup_fp64")
+
     # ------------------------------------------------------------------ API
     def logits(self, x: torch.Tensor, return_flags=False):
         """fp64 logits [N, E] (predict_logits)."""
@@ -235,7 +247,7 @@ class DevicePredictor:
             flags, flist, fcount = self._k1(xb, logits=lg)
             out64.copy_(lg)
             a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, logits64=out64)
-            check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
+            self._fixup(a, n)
         else:
             code = MOEP_F64 if x.dtype == torch.float64 else MOEP_BF16
             xs = x if code == MOEP_F64 or x.dtype == torch.bfloat16 else x.to(torch.float64)
@@ -257,11 +269,12 @@ class DevicePredictor:
             bounds = (m,) if m < self.E else ()
             flags, flist, fcount = self._k1(xb, m_sel=m, bounds=bounds, ids=ids)
             a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, m_sel=m, ids=ids)
+            self._fixup(a, n)
         else:
             xs = x if x.dtype in (torch.float64, torch.bfloat16) else x.to(torch.float64)
             code = MOEP_BF16 if xs.dtype == torch.bfloat16 else MOEP_F64
             a = self._fp64_args(xs, code, m_sel=m, ids=ids)
-        check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
+            check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
         return (ids, flags) if return_flags else ids
 
     def evaluate(self, x: torch.Tensor, truth: torch.Tensor, k: int, m_values, ids_m: int = 0,
@@ -281,7 +294,8 @@ class DevicePredictor:
         n = x.shape[0]
         truth = truth.to(device=self.device, dtype=torch.int32).contiguous()
         ncnt = 2 + 2 * len(m_values) + 2 * self.E
-        partials = torch.empty((2 * self.n_sms, ncnt), dtype=torch.int32, device=self.device)
+        # partial rows: [K1 | fix-up finish | fix-up overflow], one per SM each
+        partials = torch.empty((3 * self.n_sms, ncnt), dtype=torch.int32, device=self.device)
         counters = torch.empty(ncnt, dtype=torch.int64, device=self.device)
         ids = torch.empty((n, ids_m), dtype=torch.int32, device=self.device) if ids_m else None
         positions = sorted({1, k, *m_values, *( [ids_m] if ids_m else [])})
@@ -291,9 +305,10 @@ class DevicePredictor:
             flags, flist, fcount = self._k1(xb, m_sel=ids_m, bounds=bounds, ids=ids, truth=truth, k=k,
                                             m_values=m_values, partials=partials[: self.n_sms])
             a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, m_sel=ids_m, ids=ids,
-                                truth=truth, k=k, m_values=m_values, partials=partials[self.n_sms:])
-            check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
-            check(lib().moep_counters_reduce(ptr(partials), 2 * self.n_sms, ncnt, ptr(counters),
+                                truth=truth, k=k, m_values=m_values,
+                                partials=partials[self.n_sms: 2 * self.n_sms])
+            self._fixup(a, n, partials2=partials[2 * self.n_sms:])
+            check(lib().moep_counters_reduce(ptr(partials), 3 * self.n_sms, ncnt, ptr(counters),
                                              _stream(self.device)), "moep_counters_reduce")
             return counters, fcount, ids
         # general path: exact fp64 logits for every token, then K7 from logits

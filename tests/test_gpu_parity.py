@@ -222,3 +222,27 @@ def test_input_norm_kernel(pb, O):
         out = dev.normalize(xt, kind, g, b).double().cpu().numpy()
         ref = O.input_norm_bf16(x, kind, g, b)
         assert np.array_equal(out, ref), kind
+
+
+def test_fixup_overflow_path(pb, O):
+    """Flagged rows beyond the GEMM fix-up capacity go through the per-group fp64
+    kernel; results must be identical either way (forced tiny capacity + a wide margin)."""
+    rng = np.random.default_rng(21)
+    m = bf16_model(pb, O, "arch2", 512, 512, 64, seed=2)
+    x = O.round_bf16(rng.standard_normal((3000, 512)))
+    zref = O.predict_logits(oracle_params(m), x)
+    truth = O.top_k_batch(zref + 0.05 * rng.standard_normal(zref.shape), 6)
+    ms = [6, 10, 64]
+    oc = O.eval_counters(zref, truth, 64, ms)
+    for cap in (None, 8):
+        dev = m.to_device(tau_rel=2e-4)  # flags ~25% of tokens
+        dev.fixup_capacity = cap
+        xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+        assert np.array_equal(dev.topk(xt, 6).cpu().numpy(), O.top_k_batch(zref, 6))
+        cnt, fcount, _ = dev.evaluate(xt, torch.from_numpy(truth), 6, ms)
+        assert int(fcount.item()) > 100
+        c = pb.EvalCounters.from_array(cnt.cpu().numpy(), 6, 64, ms)
+        assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
+        assert c.top1 == oc["top1_count"] and np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
+        z = dev.logits(xt).cpu().numpy()
+        assert np.abs(z - zref).max() < LOGIT_ATOL_K1
