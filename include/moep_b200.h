@@ -218,6 +218,21 @@ typedef struct {
 } moep_optim_args;
 int moep_optim_step(const moep_optim_args* a, void* stream);
 
+/* ------------------------------------------------------------ prefetch --
+ * K8: union of the predicted expert ids of a batch (ids[0 .. n_ids)), minus
+ * experts already resident (slot_of[e] >= 0; NULL = none resident): ascending
+ * need_list[0 .. *need_count), each paired with free_slots[i] (or -1 when the
+ * cache is full). Replaces the per-token load set of pipesim.schedule's
+ * prefetch modes (pipesim.py:272-305), which the reference only models. */
+int moep_prefetch_plan(const int32_t* ids, int64_t n_ids, int32_t n_experts, const int32_t* slot_of,
+                       const int32_t* free_slots, int32_t n_free, uint8_t* mask_out, int32_t* need_list,
+                       int32_t* need_slot, int32_t* need_count, void* stream);
+/* K9: GPU-driven copy of the listed experts from mapped pinned host memory
+ * (expert e at host_mapped_store + e*expert_bytes) into cache slots. */
+int moep_gather_experts(const void* host_mapped_store, int64_t expert_bytes, const int32_t* need_list,
+                        const int32_t* need_slot, const int32_t* need_count, void* cache, int32_t n_ctas,
+                        void* stream);
+
 /* ---------------------------------------------------------------- misc -- */
 int moep_num_sms(void);
 const char* moep_version(void);

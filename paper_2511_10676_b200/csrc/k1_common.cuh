@@ -54,9 +54,12 @@ __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
 // z[EP]: this token's raw GEMM2 accumulator (no b2). Every lane of the warp
 // must call this (ballots). Mirrors predict_topk_batch / top_k_batch
 // (predictor.py:347-351, core.py:42-48) and metrics.py:159-180.
+// zrow: this thread's smem staging row (>= EP floats) used for the dynamic
+// truth-expert lookups; hist: the calling warp's private [2][EP] histogram.
 template <int EP>
 __device__ __forceinline__ void row_epilogue(const Params& p, float* z, float sumsq, int64_t row, bool valid,
-                                             uint32_t lane, int* hist, RowCounters& rc) {
+                                             uint32_t lane, int* hist, RowCounters& rc, float* zrow,
+                                             uint32_t zswz) {
   bool flagged = false;
 #pragma unroll
   for (int e = 0; e < EP; ++e) {
@@ -66,6 +69,7 @@ __device__ __forceinline__ void row_epilogue(const Params& p, float* z, float su
     } else {
       z[e] = -INFINITY;
     }
+    if (p.truth) zrow[e ^ zswz] = z[e];
   }
   int P = p.m_sel;
 #pragma unroll
@@ -139,57 +143,64 @@ __device__ __forceinline__ void row_epilogue(const Params& p, float* z, float su
       }
     }
   }
-  if (p.truth) {
-    const bool use = valid && !flagged;
-    int tr[16], te[16];
+  if (p.truth && valid && !flagged) {
+    // "truth expert t has predicted rank < m" <=> key(t) >= key(position m-1)
+    // of the sorted top list (every m the caller evaluates is < kMaxSel or == E;
+    // metrics.py:159-172). z_t is read from the per-row staging copy zrow.
+    auto thr = [&](int m, float& v, int& i) {
+      v = tv[0];
+      i = tix[0];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      tr[j] = 0;
-      te[j] = -1;
-      if (use && j < p.k) {
-        const int t = __ldg(p.truth + row * p.k + j);
-        te[j] = t;
-        float zt = 0.f;
+      for (int s = 0; s < kMaxSel; ++s)
+        if (s == m - 1) { v = tv[s]; i = tix[s]; }
+    };
+    float kv; int ki;
+    thr(p.k, kv, ki);
+    float mv[MOEP_MAX_BOUNDS];
+    int mix[MOEP_MAX_BOUNDS];
 #pragma unroll
-        for (int e = 0; e < EP; ++e)
-          if (e == t) zt = z[e];
-        int r = 0;
-#pragma unroll
-        for (int e = 0; e < EP; ++e) r += (e < p.E && key_gt(z[e], e, zt, t)) ? 1 : 0;
-        tr[j] = r;
-      }
-    }
-    if (use) {
-      rc.n += 1;
-      bool any0 = false;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) any0 |= (j < p.k && tr[j] == 0);
-      rc.top1 += any0 ? 1 : 0;
+    for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) thr(mi < p.n_m ? p.m_list[mi] : 1, mv[mi], mix[mi]);
+    int inside[MOEP_MAX_BOUNDS] = {0, 0, 0, 0};
+    bool any0 = false;
+    for (int j = 0; j < p.k; ++j) {
+      const int t = __ldg(p.truth + row * p.k + j);
+      const float zt = zrow[t ^ zswz];
+      any0 |= (t == tix[0]);
+      const bool hit = key_gt(zt, t, kv, ki) || t == ki;
+      atomicAdd(&hist[EP + t], 1);  // warp-private shared histogram
+      if (hit) atomicAdd(&hist[t], 1);
 #pragma unroll
       for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
         if (mi < p.n_m) {
           const int m = p.m_list[mi];
-          int inside = 0;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) inside += (j < p.k && tr[j] < m) ? 1 : 0;
-          rc.ov[mi] += (inside == p.k) ? 1 : 0;
-          rc.rc[mi] += inside;
+          inside[mi] += (m >= p.E || key_gt(zt, t, mv[mi], mix[mi]) || t == mix[mi]) ? 1 : 0;
         }
       }
     }
-    for (int e = 0; e < p.E; ++e) {
-      bool has = false, hit = false;
+    rc.n += 1;
+    rc.top1 += any0 ? 1 : 0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < p.k && te[j] == e) { has = true; hit = tr[j] < p.k; }
-      const uint32_t bt = __ballot_sync(0xffffffffu, has);
-      const uint32_t bh = __ballot_sync(0xffffffffu, hit);
-      if (lane == (e & 31)) {
-        hist[e] += __popc(bh);
-        hist[EP + e] += __popc(bt);
+    for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
+      if (mi < p.n_m) {
+        rc.ov[mi] += (inside[mi] == p.k) ? 1 : 0;
+        rc.rc[mi] += inside[mi];
       }
     }
   }
+}
+
+// Staging row for row_epilogue inside a 64 KB smem region (128 rows):
+// EP >= 32: stride EP with the column XOR-swizzled by the lane (conflict-free);
+// EP = 16: stride 17.
+template <int EP>
+__device__ __forceinline__ float* zstage_row(uint8_t* region, int row_in_tile, uint32_t lane, uint32_t& swz) {
+  float* base = reinterpret_cast<float*>(region);
+  if (EP >= 32) {
+    swz = lane;
+    return base + row_in_tile * EP;
+  }
+  swz = 0;
+  return base + row_in_tile * (EP + 1);
 }
 
 // Per-CTA partial counters from the 4 warps of the selecting warpgroup

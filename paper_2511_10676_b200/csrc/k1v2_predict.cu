@@ -307,7 +307,11 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(z_empty, 0);
-        k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc);
+        // The A2 buffer is idle here: WG1 cannot write the next tile's A2 before
+        // GEMM2 half 0 of its chunk 0, which needs this warpgroup's half first.
+        uint32_t zswz;
+        float* zrow = k1c::zstage_row<EP>(smem + C::OFF_A2, row_in_tile, lane, zswz);
+        k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc, zrow, zswz);
       }
     }
     if (wg == 0 && p.partials)

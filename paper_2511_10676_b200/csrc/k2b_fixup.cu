@@ -84,32 +84,80 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   // tid / 64) reads 4 consecutive k of its row; B tile [KS][TN]: thread = (hidden
   // row n = tid % 128, k-half tid / 128) reads 8 consecutive k (one 16-byte bf16
   // load). Consecutive lanes write consecutive smem columns: conflict-free.
-  auto load = [&](int buf, int k0) {
-    {
-      const int r = tid & (TM - 1), kq = tid / TM;
-      const int64_t row = rowid[r];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int kk = kq * 4 + c, k = k0 + kk;
-        As[(buf * KS + kk) * TM + r] = (row >= 0 && k < d) ? ld1<XT>(a.x, row * d + k) : 0.0;
+  // Global loads of tile kt+1 are issued into registers before the MMA-free
+  // compute of tile kt and stored (converted to fp64) after it, so their L2
+  // latency overlaps the DFMA work. Vector loads when d % 8 == 0.
+  const int ar = tid & (TM - 1), akq = tid / TM;   // A: row, k-quarter
+  const int bn = tid & (TN - 1), bkh = tid / TN;   // B: hidden row, k-half
+  const int64_t arow = rowid[ar];
+  const int bj = h0 + bn;
+  const bool vec = (d % 8) == 0;
+  // staging registers: raw bf16 words (converted at stash time) or fp64 values
+  uint32_t ua[2], ub[4];
+  double ra[(XT == MOEP_BF16) ? 1 : 4], rb[(WT == MOEP_BF16) ? 1 : 8];
+  bool a_ok, b_ok, a_vec, b_vec;
+  int ka_s, kb_s;
+  auto fetch = [&](int k0) {
+    const int ka = k0 + akq * 4, kb = k0 + bkh * 8;
+    ka_s = ka; kb_s = kb;
+    a_ok = arow >= 0 && ka < d;
+    b_ok = bj < H && kb < d;
+    a_vec = vec && a_ok;
+    b_vec = vec && b_ok;
+    if (a_vec) {
+      if constexpr (XT == MOEP_BF16) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.x) + arow * d + ka));
+        ua[0] = u.x; ua[1] = u.y;
+      } else {
+        const double2* s = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(a.x) + arow * d + ka);
+        const double2 p0 = __ldg(s), p1 = __ldg(s + 1);
+        ra[0] = p0.x; ra[1] = p0.y; ra[2] = p1.x; ra[3] = p1.y;
       }
     }
-    {
-      const int n = tid & (TN - 1), kh = tid / TN;
-      const int j = h0 + n;
+    if (b_vec) {
+      if constexpr (WT == MOEP_BF16) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.w1) +
+                                                            static_cast<int64_t>(bj) * d + kb));
+        ub[0] = u.x; ub[1] = u.y; ub[2] = u.z; ub[3] = u.w;
+      } else {
+        const double2* s = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(a.w1) +
+                                                            static_cast<int64_t>(bj) * d + kb);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int kk = kh * 8 + c, k = k0 + kk;
-        Bs[(buf * KS + kk) * TN + n] = (j < H && k < d) ? ld1<WT>(a.w1, static_cast<int64_t>(j) * d + k) : 0.0;
+        for (int c = 0; c < 4; ++c) { const double2 v = __ldg(s + c); rb[2 * c] = v.x; rb[2 * c + 1] = v.y; }
       }
     }
   };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double v;
+      if (a_vec) {
+        if constexpr (XT == MOEP_BF16) v = bf16_to_f64((c & 1) ? (ua[c >> 1] >> 16) : (ua[c >> 1] & 0xffffu));
+        else v = ra[c];
+      } else {
+        v = (arow >= 0 && ka_s + c < d) ? ld1<XT>(a.x, arow * d + ka_s + c) : 0.0;
+      }
+      As[(buf * KS + akq * 4 + c) * TM + ar] = v;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      double v;
+      if (b_vec) {
+        if constexpr (WT == MOEP_BF16) v = bf16_to_f64((c & 1) ? (ub[c >> 1] >> 16) : (ub[c >> 1] & 0xffffu));
+        else v = rb[c];
+      } else {
+        v = (bj < H && kb_s + c < d) ? ld1<WT>(a.w1, static_cast<int64_t>(bj) * d + kb_s + c) : 0.0;
+      }
+      Bs[(buf * KS + bkh * 8 + c) * TN + bn] = v;
+    }
+  };
   const int nk = (d + KS - 1) / KS;
-  load(0, 0);
+  fetch(0);
+  stash(0);
   __syncthreads();
   for (int kt = 0; kt < nk; ++kt) {
     const int buf = kt & 1;
-    if (kt + 1 < nk) load(buf ^ 1, (kt + 1) * KS);
+    if (kt + 1 < nk) fetch((kt + 1) * KS);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
       double av[4], bv[8];
@@ -130,11 +178,11 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
     }
+    if (kt + 1 < nk) stash(buf ^ 1);
     __syncthreads();
   }
-  // ---- epilogue: bias + activation -> hs [TM][TN+1]; W2^T slice -> w2s [TN][E]
+  // ---- epilogue: bias + activation -> hs [TM][TN+1]; W2^T read from L2
   double* hs = sm;                               // TM * (TN + 1)
-  double* w2s = sm + TM * (TN + 1);              // TN * E
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int jl = (j >> 1) * 32 + tx * 2 + (j & 1), jg = h0 + jl;
@@ -160,18 +208,16 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
       hs[r * (TN + 1) + jl] = hv;
     }
   }
-  for (int e = tid; e < TN * E; e += NT) {
-    const int jl = e / E, ex = e - jl * E, jg = h0 + jl;
-    w2s[e] = jg < H ? ld1<WT>(a.w2t, static_cast<int64_t>(jg) * E + ex) : 0.0;
-  }
   __syncthreads();
-  // partial z for this hidden tile: thread owns (row, expert) pairs, fixed j order
+  // partial z for this hidden tile: thread owns (row, expert) pairs, fixed j order;
+  // consecutive threads read consecutive experts of a W2^T row (coalesced).
+  const int jn = (H - h0) < TN ? (H - h0) : TN;
   for (int o = tid; o < TM * E; o += NT) {
     const int r = o / E, e = o - r * E;
     if (rowid[r] < 0) continue;
     double s = 0.0;
     const double* hr = hs + r * (TN + 1);
-    for (int jl = 0; jl < TN; ++jl) s = fma(hr[jl], w2s[jl * E + e], s);
+    for (int jl = 0; jl < jn; ++jl) s = fma(hr[jl], ld1<WT>(a.w2t, static_cast<int64_t>(h0 + jl) * E + e), s);
     part[((r0 + r) * ntile_h + blockIdx.y) * E + e] = s;
   }
 }
@@ -270,7 +316,7 @@ extern "C" int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t
   const int E = a->n_experts;
   const int ntile_h = (a->hidden + TN - 1) / TN;
   const size_t smem_main = sizeof(double) * 2 * KS * (TM + TN);
-  const size_t smem_epi = sizeof(double) * (TM * (TN + 1) + TN * E);
+  const size_t smem_epi = sizeof(double) * (TM * (TN + 1));
   const size_t smem = smem_main > smem_epi ? smem_main : smem_epi;
   if (smem > 200 * 1024) return MOEP_EUNSUPPORTED;
   const bool xb = a->x_dtype == MOEP_BF16, wb = a->w_dtype == MOEP_BF16;
