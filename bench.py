@@ -155,6 +155,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=TOKENS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-prefetch", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -233,6 +234,9 @@ def main():
             cpu = cpu_baseline(layers[0][0], layers[0][2], layers[0][3], n_sample=32768)
     if not args.no_e2e:
         e2e = e2e_arm(layers, args, world, dev)
+    prefetch = None
+    if rank == 0 and not args.no_prefetch:
+        prefetch = prefetch_arm(layers[0][1], layers[0][2], dev)
 
     if rank == 0:
         line = {
@@ -261,6 +265,7 @@ def main():
                                 "overprov10": c0.overprov[10] / c0.n},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "prefetch": prefetch,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -312,6 +317,66 @@ def cpu_baseline(model, x, truth, n_sample=32768):
     return {"value": n_sample / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"{n_sample} tokens of layer 0: predict_logits + top_k_batch(6) + evaluate_predictions "
                       f"(oracle/oracle.py numpy fp64, OpenBLAS all threads), {dt:.2f} s"}
+
+
+def prefetch_arm(dp, x, dev, batches=(1, 8, 32, 128, 256)):
+    """Predicted-expert prefetch (BASELINE configs[4]): DSV2L expert blobs
+    (17,301,504 B) from pinned host memory into a device cache, for the union of
+    the predicted top-6 sets of B tokens, vs the measured host-link H2D peak.
+    Also the attention overlap at B=1: stall = max(0, load_end - attention_end)."""
+    import torch
+    import torch.nn.functional as F
+    from paper_2511_10676_b200 import prefetch as pf
+    E = dp.E
+    peak = pf.measure_h2d_peak(1 << 30, reps=5, device=dev)
+    store = pf.ExpertStore(E, pf.DSV2L_EXPERT_BYTES)
+    cache = pf.ExpertCache(E, pf.DSV2L_EXPERT_BYTES, E, device=dev)
+    p = pf.Prefetcher(store, cache)
+    out = {"h2d_peak_gbs": peak, "peak_kind": "pinned cudaMemcpyAsync 1 GiB, best of 5 (measured)",
+           "expert_bytes": pf.DSV2L_EXPERT_BYTES, "sweep": []}
+
+    def timed(fn):
+        cache.reset()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(p.copy)
+        fn()
+        b.record(p.copy)
+        b.synchronize()
+        return a.elapsed_time(b)
+
+    for B in batches:
+        ids = dp.topk(x[:B], K_ACT)
+        for path in ("copy_engine", "sm_gather"):
+            fn = (lambda: p.load_copy_engine(ids)) if path == "copy_engine" else (lambda: p.load_sm_gather(ids, 148))
+            timed(fn)  # warm
+            ms = min(timed(fn) for _ in range(3))
+            n = int(p.need_count.item())
+            gbs = n * pf.DSV2L_EXPERT_BYTES / (ms / 1e3) / 1e9
+            out["sweep"].append({"batch_tokens": B, "path": path, "experts_loaded": n,
+                                 "bytes": n * pf.DSV2L_EXPERT_BYTES, "ms": ms, "gbs": gbs, "frac": gbs / peak})
+    # overlap with an attention stand-in (decode, B=1: 16 q heads, 16 kv heads, head_dim 128,
+    # 4096 cached tokens; DeepSeek-V2-Lite MLA is approximated by plain SDPA)
+    q = torch.randn(1, 16, 1, 128, device=dev, dtype=torch.bfloat16)
+    kv = torch.randn(1, 16, 4096, 128, device=dev, dtype=torch.bfloat16)
+    ids = dp.topk(x[:1], K_ACT)
+    main = torch.cuda.current_stream(dev)
+    cache.reset()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t_attn, t_load = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(main)
+    p.copy.wait_event(t0)
+    p.load_sm_gather(ids, 148)
+    t_load.record(p.copy)
+    F.scaled_dot_product_attention(q, kv, kv)  # this layer's attention: the prefetch window
+    t_attn.record(main)
+    torch.cuda.synchronize()
+    la, ll = t0.elapsed_time(t_attn), t0.elapsed_time(t_load)
+    out["overlap_b1"] = {"attention_ms": la, "load_ms": ll, "stall_ms": max(0.0, ll - la),
+                         "note": "one decode SDPA (16 heads x 4096 cached tokens) as the window; "
+                                 "stall = max(0, load_end - attention_end) as pipesim.py:281-285"}
+    return out
 
 
 def e2e_arm(layers, args, world, dev):
