@@ -221,17 +221,18 @@ int moep_optim_step(const moep_optim_args* a, void* stream);
 /* arch1 training (fp64): batch-norm with batch statistics + running update,
  * GELU-tanh and Philox4x64-10 dropout identical to numpy's Generator.random
  * keyed (seed << 64) + step (predictor.py:70-72, 208-237); rows_dot is the
- * fp64 GEMM2 z = h . W^T + b; bn_backward is predictor.py:280-297. */
+ * fp64 GEMM2 z = h . W^T + b; bn_backward is predictor.py:280-297. training = 0
+ * gives the eval-mode forms (running statistics, no dropout, predictor.py:221-224, 292-296). */
 int moep_bn_forward(const double* a, int64_t n, int32_t hidden, const double* scale, const double* shift,
                     double* run_mean, double* run_var, double momentum, double eps, double dropout_rate,
                     uint64_t dropout_seed, uint64_t dropout_step, const uint8_t* given_mask, double* a_hat,
-                    double* bn_out, double* keep, double* h, double* inv_std, void* stream);
+                    double* bn_out, double* keep, double* h, double* inv_std, int32_t training, void* stream);
 int moep_rows_dot(const double* h, const double* w, const double* b, int64_t n, int32_t hidden, int32_t n_out,
                   double* z, void* stream);
 int moep_bn_backward(const double* dz, const double* w2, int64_t n, int32_t hidden, int32_t n_experts,
                      const double* h, const double* keep, const double* bn_out, const double* a_hat,
                      const double* inv_std, const double* scale, double* da, double* dw2, double* db1,
-                     double* dscale, double* dshift, void* stream);
+                     double* dscale, double* dshift, int32_t training, void* stream);
 
 /* ------------------------------------------------------------ prefetch --
  * K8: union of the predicted expert ids of a batch (ids[0 .. n_ids)), minus

@@ -397,7 +397,7 @@ def teacher_scores(x, gate_w):
 
 # ------------------------------------------------------------ train loop
 def train_arch2(acts, scores, topk, k, *, hidden=32, batch_size=64, epochs=1, lr=1e-3, optimizer="adam",
-                seed=0, eval_fraction=0.1, loss=None, overprov_m=None, max_steps=None):
+                seed=0, eval_fraction=0.1, loss=None, overprov_m=None, max_steps=None, arch="arch2"):
     """Restatement of trainer.train for arch2 (trainer.py:131-204): Philox
     shuffle/split, labels from the fp64 cast of the fp32 scores, minibatch
     forward / loss_and_grad / backward / optimizer, held-out eval per epoch.
@@ -413,7 +413,9 @@ def train_arch2(acts, scores, topk, k, *, hidden=32, batch_size=64, epochs=1, lr
     x_tr = acts[tr_idx].astype(np.float64)
     lab = batch_labels(scores[tr_idx].astype(np.float64), k)
     x_ev, tk_ev = acts[ev_idx].astype(np.float64), topk[ev_idx]
-    p = init_params("arch2", d, hidden, e, seed=seed)
+    p = init_params(arch, d, hidden, e, seed=seed)
+    drop = {"seed": seed, "step": 0}
+    names = ("w1", "b1", "w2", "b2") + (("bn_scale", "bn_shift") if arch == "arch1" else ())
     state, t, steps, rows = {}, 0, 0, []
     for _ in range(epochs):
         order = rng.permutation(x_tr.shape[0])
@@ -421,10 +423,13 @@ def train_arch2(acts, scores, topk, k, *, hidden=32, batch_size=64, epochs=1, lr
         for start in range(0, x_tr.shape[0], batch_size):
             b = order[start: start + batch_size]
             lb = {kk: v[b] for kk, v in lab.items()}
-            z, cache = forward_eval(p, x_tr[b])  # arch2 train forward == eval forward
+            if arch == "arch1":
+                z, cache = forward_train_arch1(p, x_tr[b], drop)
+            else:
+                z, cache = forward_eval(p, x_tr[b])  # arch2 train forward == eval forward
             lv, dz = loss_and_grad(loss, z, lb)
-            g = backward_eval(p, cache, dz)
-            g = {kk: g[kk] for kk in ("w1", "b1", "w2", "b2")}
+            g = backward_train_arch1(p, cache, dz) if arch == "arch1" else backward_eval(p, cache, dz)
+            g = {kk: g[kk] for kk in names}
             t += 1
             if optimizer == "adam":
                 adam_step(p, g, state, t, lr=lr)
@@ -437,3 +442,53 @@ def train_arch2(acts, scores, topk, k, *, hidden=32, batch_size=64, epochs=1, lr
         res = evaluate_predictions(predict_logits(p, x_ev), tk_ev, e, [m_over])
         rows.append((loss_sum / x_tr.shape[0], res["exact_match"], res["top1"], res["overprov"][m_over]))
     return p, rows, steps
+
+
+# ------------------------------------------------ arch1 train mode (BN + dropout)
+def forward_train_arch1(p, x, state, dropout_mask=None, momentum=0.1, rate=0.1):
+    """Train-mode arch1 forward (predictor.py:208-237): batch statistics, running
+    update (unbiased variance), Philox(seed << 64 + step) dropout. `state` holds
+    'seed' and 'step' (advanced when a mask is drawn). Mutates p's bn_mean/bn_var."""
+    x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    a = x @ p["w1"].T + p["b1"]
+    mu, var = a.mean(axis=0), a.var(axis=0)
+    inv_std = 1.0 / np.sqrt(var + p.get("bn_eps", 1e-5))
+    a_hat = (a - mu) * inv_std
+    n = a.shape[0]
+    var_run = var * (n / (n - 1)) if n > 1 else var
+    p["bn_mean"] *= 1.0 - momentum
+    p["bn_mean"] += momentum * mu
+    p["bn_var"] *= 1.0 - momentum
+    p["bn_var"] += momentum * var_run
+    bn_out = p["bn_scale"] * a_hat + p["bn_shift"]
+    g = gelu_tanh(bn_out)
+    if rate > 0:
+        if dropout_mask is None:
+            key = ((int(state["seed"]) & 0xFFFFFFFFFFFFFFFF) << 64) + int(state["step"])
+            dropout_mask = np.random.Generator(np.random.Philox(key=key)).random(g.shape) >= rate
+            state["step"] += 1
+        keep = dropout_mask.astype(np.float64) / (1.0 - rate)
+        h = g * keep
+    else:
+        keep = None
+        h = g
+    cache = {"x": x, "a": a, "a_hat": a_hat, "inv_std": inv_std, "bn_out": bn_out, "keep": keep, "h": h}
+    return h @ p["w2"].T + p["b2"], cache
+
+
+def backward_train_arch1(p, cache, dz):
+    """predictor.py:261-297 with training=True (batch-statistics backward)."""
+    dz = np.atleast_2d(np.asarray(dz, dtype=np.float64))
+    g = {"w2": dz.T @ cache["h"], "b2": dz.sum(axis=0)}
+    dh = dz @ p["w2"]
+    dg = dh * cache["keep"] if cache["keep"] is not None else dh
+    dbn = dg * gelu_tanh_grad(cache["bn_out"])
+    g["bn_scale"] = (dbn * cache["a_hat"]).sum(axis=0)
+    g["bn_shift"] = dbn.sum(axis=0)
+    da_hat = dbn * p["bn_scale"]
+    n = cache["a"].shape[0]
+    a_hat = cache["a_hat"]
+    da = cache["inv_std"] / n * (n * da_hat - da_hat.sum(axis=0) - a_hat * (da_hat * a_hat).sum(axis=0))
+    g["w1"] = da.T @ cache["x"]
+    g["b1"] = da.sum(axis=0)
+    return g

@@ -83,9 +83,9 @@ _SIGS = {
     "moep_act_backward": [vp, vp, vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
     "moep_optim_step": [C.POINTER(OptimArgs), vp],
     "moep_bn_forward": [vp, i64, i32, vp, vp, vp, vp, f64, f64, f64, C.c_uint64, C.c_uint64, vp, vp, vp, vp,
-                        vp, vp, vp],
+                        vp, vp, i32, vp],
     "moep_rows_dot": [vp, vp, vp, i64, i32, i32, vp, vp],
-    "moep_bn_backward": [vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+    "moep_bn_backward": [vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp],
     "moep_prefetch_plan": [vp, i64, i32, vp, vp, i32, vp, vp, vp, vp, vp],
     "moep_gather_experts": [vp, i64, vp, vp, vp, vp, i32, vp],
     "moep_num_sms": [],

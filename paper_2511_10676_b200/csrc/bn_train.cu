@@ -56,23 +56,31 @@ __global__ void bn_forward_kernel(const double* __restrict__ a, int64_t n, int H
                                   double* __restrict__ run_var, double momentum, double eps, double rate,
                                   uint64_t key_step, uint64_t key_seed, const uint8_t* __restrict__ given_mask,
                                   double* __restrict__ a_hat, double* __restrict__ bn_out, double* __restrict__ keep,
-                                  double* __restrict__ h, double* __restrict__ inv_std_out) {
+                                  double* __restrict__ h, double* __restrict__ inv_std_out, int training) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= H) return;
-  double s = 0.0;
-  for (int64_t r = 0; r < n; ++r) s += a[r * H + j];
-  const double mu = s / static_cast<double>(n);
-  double v = 0.0;
-  for (int64_t r = 0; r < n; ++r) {
-    const double c = a[r * H + j] - mu;
-    v += c * c;
+  double mu, inv_std;
+  if (training) {
+    double s = 0.0;
+    for (int64_t r = 0; r < n; ++r) s += a[r * H + j];
+    mu = s / static_cast<double>(n);
+    double v = 0.0;
+    for (int64_t r = 0; r < n; ++r) {
+      const double c = a[r * H + j] - mu;
+      v += c * c;
+    }
+    const double var = v / static_cast<double>(n);
+    inv_std = 1.0 / sqrt(var + eps);
+    const double var_run = n > 1 ? var * (static_cast<double>(n) / static_cast<double>(n - 1)) : var;
+    run_mean[j] = __dadd_rn(__dmul_rn(run_mean[j], 1.0 - momentum), __dmul_rn(momentum, mu));
+    run_var[j] = __dadd_rn(__dmul_rn(run_var[j], 1.0 - momentum), __dmul_rn(momentum, var_run));
+  } else {
+    // eval mode: running statistics, no dropout (predictor.py:221-224, 236-237)
+    mu = run_mean[j];
+    inv_std = 1.0 / sqrt(run_var[j] + eps);
+    rate = 0.0;
   }
-  const double var = v / static_cast<double>(n);
-  const double inv_std = 1.0 / sqrt(var + eps);
   inv_std_out[j] = inv_std;
-  const double var_run = n > 1 ? var * (static_cast<double>(n) / static_cast<double>(n - 1)) : var;
-  run_mean[j] = run_mean[j] * (1.0 - momentum) + momentum * mu;
-  run_var[j] = run_var[j] * (1.0 - momentum) + momentum * var_run;
   const double sc = scale[j], sh = shift[j];
   const double inv_keep = rate > 0.0 ? 1.0 / (1.0 - rate) : 1.0;
   for (int64_t r = 0; r < n; ++r) {
@@ -113,7 +121,7 @@ __global__ void bn_backward_kernel(const double* __restrict__ dz, const double* 
                                    const double* __restrict__ bn_out, const double* __restrict__ a_hat,
                                    const double* __restrict__ inv_std, const double* __restrict__ scale,
                                    double* __restrict__ da, double* __restrict__ dw2, double* __restrict__ db1,
-                                   double* __restrict__ dscale, double* __restrict__ dshift) {
+                                   double* __restrict__ dscale, double* __restrict__ dshift, int training) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= H) return;
   const double sc = scale[j];
@@ -147,7 +155,8 @@ __global__ void bn_backward_kernel(const double* __restrict__ dz, const double* 
   for (int64_t r = 0; r < n; ++r) {
     const int64_t i = r * H + j;
     const double dah = da[i] * sc;
-    const double v = is / nn * (nn * dah - sum_dah - a_hat[i] * sum_dah_ah);
+    // train: through the batch statistics; eval: da = da_hat * inv_std (predictor.py:292-296)
+    const double v = training ? is / nn * (nn * dah - sum_dah - a_hat[i] * sum_dah_ah) : dah * is;
     da[i] = v;
     s_da += v;
   }
@@ -162,12 +171,12 @@ extern "C" {
 int moep_bn_forward(const double* a, int64_t n, int32_t hidden, const double* scale, const double* shift,
                     double* run_mean, double* run_var, double momentum, double eps, double dropout_rate,
                     uint64_t dropout_seed, uint64_t dropout_step, const uint8_t* given_mask, double* a_hat,
-                    double* bn_out, double* keep, double* h, double* inv_std, void* stream) {
+                    double* bn_out, double* keep, double* h, double* inv_std, int32_t training, void* stream) {
   if (n <= 0 || hidden <= 0) return MOEP_ESHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   moep::bn::bn_forward_kernel<<<(hidden + 127) / 128, 128, 0, st>>>(
       a, n, hidden, scale, shift, run_mean, run_var, momentum, eps, dropout_rate, dropout_step, dropout_seed,
-      given_mask, a_hat, bn_out, keep, h, inv_std);
+      given_mask, a_hat, bn_out, keep, h, inv_std, training);
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }
 
@@ -184,12 +193,12 @@ int moep_rows_dot(const double* h, const double* w, const double* b, int64_t n, 
 int moep_bn_backward(const double* dz, const double* w2, int64_t n, int32_t hidden, int32_t n_experts,
                      const double* h, const double* keep, const double* bn_out, const double* a_hat,
                      const double* inv_std, const double* scale, double* da, double* dw2, double* db1,
-                     double* dscale, double* dshift, void* stream) {
+                     double* dscale, double* dshift, int32_t training, void* stream) {
   if (n <= 0 || hidden <= 0 || n_experts <= 0) return MOEP_ESHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   moep::bn::bn_backward_kernel<<<(hidden + 127) / 128, 128, 0, st>>>(dz, w2, n, hidden, n_experts, h, keep, bn_out,
                                                                     a_hat, inv_std, scale, da, dw2, db1, dscale,
-                                                                    dshift);
+                                                                    dshift, training);
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }
 

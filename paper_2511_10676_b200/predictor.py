@@ -169,23 +169,26 @@ def predict_topk(model: PredictorModel, x, m: int) -> ExpertSelection:
 def _trainer_fp64(model):
     from .losses import LossSpec
     from .train_engine import DeviceTrainer
-    if model.arch != "arch2":
-        raise NotImplementedError("device forward/backward in train mode is implemented for arch2 "
-                                  "(arch1 batch-norm training is listed as a gap in DESIGN.md)")
     return DeviceTrainer(model, LossSpec(), precision="fp64")
 
 
 def forward(model: PredictorModel, x, *, dropout_mask=None):
     """Predictor logits (predictor.py:243-258). Eval mode == predict_logits; train
-    mode runs the fp64 device forward (K2 with pre-activation output) and keeps
-    the intermediates for a paired backward()."""
+    mode runs the fp64 device forward (K2 with pre-activation output; arch1 adds
+    batch statistics, the running-stat update and the Philox dropout stream) and
+    keeps the intermediates for a paired backward()."""
     if model.mode != "train":
         return predict_logits(model, x)
     batch, single, is_t = _as_batch(model, x)
     tr = _trainer_fp64(model)
-    z, a_pre, xd = tr.forward(batch.to("cuda"))
+    z, cache, xd = tr.forward(batch.to("cuda"), dropout_mask=dropout_mask, training=True)
+    if model.arch == "arch1":
+        # the reference mutates the running statistics and the dropout counter in place
+        model.bn_mean[...] = tr.run_mean.cpu().numpy()
+        model.bn_var[...] = tr.run_var.cpu().numpy()
+        model._dropout_step = tr.dropout_step
     host_x = batch.detach().cpu().numpy().astype(np.float64) if is_t else batch.numpy()
-    model._cache = {"x": host_x, "a": a_pre, "x_dev": xd, "trainer": tr}
+    model._cache = {"x": host_x, "cache": cache, "x_dev": xd, "trainer": tr}
     out = z if is_t else z.cpu().numpy()
     return out[0] if single else out
 
@@ -205,12 +208,12 @@ def backward(model: PredictorModel, x, dlogits) -> dict:
         host_x = batch.detach().cpu().numpy().astype(np.float64) if is_t else batch.numpy()
         if c is None or c["x"].shape != host_x.shape or not np.array_equal(c["x"], host_x):
             raise UsageError("train-mode backward requires a paired forward on the same input")
-        tr, a_pre, xd = c["trainer"], c["a"], c["x_dev"]
+        tr, cache, xd = c["trainer"], c["cache"], c["x_dev"]
     else:
         tr = _trainer_fp64(model)
-        _, a_pre, xd = tr.forward(batch.to("cuda"))
-    tr.backward(xd, a_pre, dz.contiguous())
-    names = ("w1", "w2", "b1", "b2")
+        _, cache, xd = tr.forward(batch.to("cuda"), training=False)
+    tr.backward(xd, cache, dz.contiguous())
+    names = ("w1", "w2", "b1", "b2", "bn_scale", "bn_shift")[: len(tr.sizes)]
     return {n: tr.view(tr.grad, i).clone().cpu().numpy() for i, n in enumerate(names)}
 
 

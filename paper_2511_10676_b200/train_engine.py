@@ -107,7 +107,7 @@ class DeviceTrainer:
         check(lib().moep_predict_fp64(A, _stream(self.dev)), "moep_predict_fp64")
         return a_pre
 
-    def forward(self, x, dropout_mask=None):
+    def forward(self, x, dropout_mask=None, training=True):
         """Train-mode forward: logits [N, E], the cache the backward needs, and
         the activations actually used."""
         n = x.shape[0]
@@ -142,12 +142,13 @@ class DeviceTrainer:
                                     ptr(self.run_mean), ptr(self.run_var), self.bn_momentum, self.bn_eps,
                                     self.dropout_rate, self.dropout_seed, self.dropout_step, ptr(mask),
                                     ptr(buf["a_hat"]), ptr(buf["bn_out"]), ptr(buf["keep"]), ptr(buf["h"]),
-                                    ptr(inv_std), _stream(self.dev)), "moep_bn_forward")
-        if self.dropout_rate > 0 and dropout_mask is None:
+                                    ptr(inv_std), int(training), _stream(self.dev)), "moep_bn_forward")
+        if training and self.dropout_rate > 0 and dropout_mask is None:
             self.dropout_step += 1  # the reference draws one mask per train forward (predictor.py:228-230)
         check(lib().moep_rows_dot(ptr(buf["h"]), ptr(self.view(self.flat, 1)), ptr(self.view(self.flat, 3)), n, H,
                                   self.E, ptr(z), _stream(self.dev)), "moep_rows_dot")
         buf["inv_std"] = inv_std
+        buf["training"] = training
         return z, buf, x64
 
     # --------------------------------------------------------- backward
@@ -162,7 +163,7 @@ class DeviceTrainer:
                                          ptr(cache["inv_std"]), ptr(self.view(self.flat, 4)), ptr(da),
                                          ptr(self.view(self.grad, 1)), ptr(self.view(self.grad, 2)),
                                          ptr(self.view(self.grad, 4)), ptr(self.view(self.grad, 5)),
-                                         _stream(self.dev)), "moep_bn_backward")
+                                         int(cache.get("training", True)), _stream(self.dev)), "moep_bn_backward")
             torch.sum(dz, dim=0, out=self.view(self.grad, 3))
         else:
             n_slices = max(1, min(64, n // 256))

@@ -118,6 +118,71 @@ def test_train_fp64_matches_oracle_loop(pb, O, family):
         assert (ours.exact_match, ours.top1, ours.overprov) == pytest.approx(ref[1:], abs=0)
 
 
+def test_backward_golden_arch1_eval(pb, golden):
+    g = golden("predictor")
+    pre = "small_arch1_"
+    m = pb.PredictorModel("arch1", g[pre + "w1"], g[pre + "b1"], g[pre + "w2"], g[pre + "b2"],
+                          **{n: g[pre + n] for n in ("bn_scale", "bn_shift", "bn_mean", "bn_var")})
+    grads = pb.backward(m, g[pre + "x"], g[pre + "dz"])
+    for name in ("w1", "b1", "w2", "b2", "bn_scale", "bn_shift"):
+        assert np.allclose(grads[name], g[pre + "grad_" + name], rtol=1e-10, atol=1e-12), name
+
+
+def _perturbed_arch1(pb, rng):
+    m = pb.init_model("arch1", 8, 16, 8, seed=7)
+    for p in m.param_dict().values():
+        p += 0.3 * rng.standard_normal(p.shape)
+    m.bn_mean += 0.1 * rng.standard_normal(16)
+    m.bn_var = np.abs(m.bn_var + 0.2 * rng.standard_normal(16))
+    return m
+
+
+def _oracle_params(m):
+    return {"arch": "arch1", "w1": m.w1.copy(), "b1": m.b1.copy(), "w2": m.w2.copy(), "b2": m.b2.copy(),
+            "bn_scale": m.bn_scale.copy(), "bn_shift": m.bn_shift.copy(), "bn_mean": m.bn_mean.copy(),
+            "bn_var": m.bn_var.copy(), "bn_eps": m.bn_eps}
+
+
+def test_arch1_train_forward_backward_vs_oracle(pb, O, rng):
+    """BN batch statistics, running update, Philox dropout stream and the BN-train backward."""
+    m = _perturbed_arch1(pb, rng)
+    p = _oracle_params(m)
+    state = {"seed": m.dropout_seed, "step": 0}
+    m.train()
+    x = rng.standard_normal((12, 8))
+    for step in range(3):  # consecutive forwards draw consecutive dropout masks
+        z = pb.forward(m, x)
+        zr, cache = O.forward_train_arch1(p, x, state)
+        assert np.allclose(z, zr, rtol=1e-11, atol=1e-12), step
+        assert np.allclose(m.bn_mean, p["bn_mean"], rtol=1e-13, atol=1e-15)
+        assert np.allclose(m.bn_var, p["bn_var"], rtol=1e-13, atol=1e-15)
+        assert m._dropout_step == state["step"]
+    dz = rng.standard_normal(z.shape)
+    g = pb.backward(m, x, dz)
+    gr = O.backward_train_arch1(p, cache, dz)
+    for name in ("w1", "b1", "w2", "b2", "bn_scale", "bn_shift"):
+        assert np.allclose(g[name], gr[name], rtol=1e-9, atol=1e-12), name
+    # a supplied mask is used verbatim (predictor.py:243-245)
+    mask = rng.random((12, 16)) >= 0.1
+    z = pb.forward(m, x, dropout_mask=mask)
+    zr, _ = O.forward_train_arch1(p, x, state, dropout_mask=mask)
+    assert np.allclose(z, zr, rtol=1e-11, atol=1e-12)
+
+
+def test_train_arch1_fp64_matches_oracle_loop(pb, O):
+    acts, scores, topk = _dataset(O, n=600)
+    cfg = pb.TrainConfig(loss=pb.LossSpec(family="ranking"), arch="arch1", hidden=32, batch_size=64, epochs=2,
+                         seed=3, eval_fraction=0.2, precision="fp64")
+    model, report = pb.train(cfg, pb.TraceFile(16, 8, 2, acts, scores, topk))
+    p, rows, _ = O.train_arch2(acts, scores, topk, 2, hidden=32, batch_size=64, epochs=2, seed=3,
+                               eval_fraction=0.2, loss={"family": "ranking"}, arch="arch1")
+    for name in ("w1", "b1", "w2", "b2", "bn_scale", "bn_shift", "bn_mean", "bn_var"):
+        assert np.allclose(getattr(model, name), p[name], rtol=1e-8, atol=1e-10), name
+    for ours, ref in zip(report.epochs, rows):
+        assert ours.train_loss == pytest.approx(ref[0], rel=1e-9)
+        assert (ours.exact_match, ours.top1, ours.overprov) == pytest.approx(ref[1:], abs=0)
+
+
 def test_train_c4_shape_fp32_step_within_tolerance(pb, O):
     """Phi-mini shape (d=4096, h=2048, E=16, k=2), arch2 + ranking, one fp32 tensor-core
     step vs the fp64 oracle step: loss rel 1e-3, parameter update rel 2e-2."""
