@@ -51,6 +51,19 @@ __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// non-blocking probe of an mbarrier phase
+__device__ __forceinline__ bool test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
 // z[EP]: this token's raw GEMM2 accumulator (no b2). Every lane of the warp
 // must call this (ballots). Mirrors predict_topk_batch / top_k_batch
 // (predictor.py:347-351, core.py:42-48) and metrics.py:159-180.

@@ -157,26 +157,44 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         const uint32_t a_base = smem_u32(smem + C::OFF_A), b_base = smem_u32(smem + C::OFF_B);
         const uint32_t a2_base = smem_u32(smem + C::OFF_A2), w2_base = smem_u32(smem + C::OFF_W2);
         uint32_t stage = 0, phase = 0, gc = 0, ti = 0;
-        auto gemm2 = [&](int cc, uint32_t chunk_id) {
-          if (cc == 0) wait(z_empty, (ti & 1) ^ 1);
-          wait(w2_full, chunk_id & 1);
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            wait(&a2_full[half], chunk_id & 1);
+        // GEMM2 of a chunk is issued half by half as soon as its A2 half is
+        // ready, interleaved between the next chunk's GEMM1 K-blocks (polled
+        // without blocking), so the epilogue's second half never waits for a
+        // whole GEMM1 K-loop and the accumulator drains promptly.
+        int p_cc = 0, p_half = 2;      // pending GEMM2: chunk-in-tile, next half (2 = none)
+        uint32_t p_id = 0, p_ti = 0;   // its global chunk index and tile iteration
+        auto pump = [&](bool block) {
+          while (p_half < 2) {
+            if (p_half == 0) {
+              if (p_cc == 0) {
+                if (block) wait(z_empty, (p_ti & 1) ^ 1);
+                else if (!k1c::test(z_empty, (p_ti & 1) ^ 1)) return;
+              }
+              if (block) wait(w2_full, p_id & 1);
+              else if (!k1c::test(w2_full, p_id & 1)) return;
+            }
+            if (block) wait(&a2_full[p_half], p_id & 1);
+            else if (!k1c::test(&a2_full[p_half], p_id & 1)) return;
             tc_fence_after();
+            const int half = p_half;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const int at = kk >> 2, w = kk & 3;
               const uint64_t bd = sdesc_k_sw128(w2_base + (half * 2 + at) * C::W2_ATOM + w * 32);
               const uint64_t ahi = sdesc_k_sw128(a2_base + at * C::ATOM + w * 32);
               const uint64_t alo = sdesc_k_sw128(a2_base + (2 + at) * C::ATOM + w * 32);
-              umma_bf16_cg2(tmem + C::ZCOL, ahi, bd, idesc2, (cc | half | kk) != 0);
+              umma_bf16_cg2(tmem + C::ZCOL, ahi, bd, idesc2, (p_cc | half | kk) != 0);
               umma_bf16_cg2(tmem + C::ZCOL, alo, bd, idesc2, 1u);
             }
-            umma_commit_mc(half == 0 ? a2_emptyA : a2_emptyB, 0x3);
+            if (half == 0) {
+              umma_commit_mc(a2_emptyA, 0x3);
+            } else {
+              umma_commit_mc(a2_emptyB, 0x3);
+              umma_commit_mc(w2_empty, 0x3);
+              if (p_cc == nchunks - 1) umma_commit_mc(z_full, 0x3);
+            }
+            ++p_half;
           }
-          umma_commit_mc(w2_empty, 0x3);
-          if (cc == nchunks - 1) umma_commit_mc(z_full, 0x3);
         };
         for (int tile = pair; tile < num_tiles; tile += n_pairs, ++ti) {
           for (int c = 0; c < nchunks; ++c, ++gc) {
@@ -193,12 +211,14 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
               }
               umma_commit_mc(&empty[stage], 0x3);
               if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+              pump(false);
             }
             umma_commit_mc(acc_full, 0x3);
-            if (c > 0) gemm2(c - 1, gc - 1);
+            pump(true);  // previous chunk's GEMM2 fully issued before this one is queued
+            p_cc = c; p_half = 0; p_id = gc; p_ti = ti;
           }
-          gemm2(nchunks - 1, gc - 1);
         }
+        pump(true);
       }
     }
   } else {
