@@ -116,13 +116,24 @@ typedef struct {
 
 int moep_predict_fp64(const moep_fp64_args* a, void* stream);
 
-/* K2 fast path for the flagged rows: register-blocked fp64 GEMM over the rows
- * in rows[0 .. min(*row_count, capacity)) with per-hidden-tile partial logits
- * in `scratch` (capacity * ceil(hidden/128) * E doubles), then a per-token
- * finish kernel; rows beyond the capacity go through moep_predict_fp64 with
- * their evaluation partials in partials2 ([moep_num_sms(), n_counters]). */
+/* K2 fast path for the flagged rows (rows / row_count required): the rows in
+ * rows[0 .. min(*row_count, capacity)) are recomputed in fp64 with
+ * per-hidden-tile partial logits in `scratch`, by the split-hidden kernel of
+ * moep_decode_fp64 when *row_count <= 256 and by a register-blocked fp64 GEMM
+ * otherwise (decided on the device), then a per-token finish kernel; rows
+ * beyond the capacity go through moep_predict_fp64 with their evaluation
+ * partials in partials2 ([moep_num_sms(), n_counters]).
+ * scratch: max(capacity * ceil(hidden/128), min(capacity, 256) * ceil(hidden/16)) * E doubles. */
 int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t capacity, int32_t* partials2,
                     void* stream);
+
+/* Decode-batch predictor (serving: a few tokens per step), exact fp64 for all
+ * N rows (rows must be NULL): the hidden dimension is split over
+ * ceil(hidden/16) CTAs so the weight stream is spread over the whole GPU,
+ * then the same finish kernel as the fix-up. Same outputs as
+ * moep_predict_fp64 (predict_topk_batch, predictor.py:337-351).
+ * scratch: N * ceil(hidden/16) * E doubles. No host synchronisation. */
+int moep_decode_fp64(const moep_fp64_args* a, double* scratch, void* stream);
 
 /* ------------------------------------------------------------------ K7 --
  * Evaluation / selection from given logits (fp64 or fp32), exact compares.

@@ -72,6 +72,7 @@ _SIGS = {
     "moep_predict_bf16": [C.POINTER(PredictArgs), vp],
     "moep_predict_fp64": [C.POINTER(Fp64Args), vp],
     "moep_fixup_fp64": [C.POINTER(Fp64Args), vp, i64, vp, vp],
+    "moep_decode_fp64": [C.POINTER(Fp64Args), vp, vp],
     "moep_eval_logits": [vp, i32, i64, i32, vp, i32, i32, vp, vp, vp],
     "moep_topk_logits": [vp, i32, i64, i32, i32, vp, vp],
     "moep_rank_order": [vp, i32, i64, i32, vp, vp],

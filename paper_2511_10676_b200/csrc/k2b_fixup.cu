@@ -19,11 +19,13 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace moep {
 namespace k2b {
 
 constexpr int TM = 64, TN = 128, KS = 16;
+constexpr int DEC_ROWS_MAX = 256;  // fix-up: flagged counts up to this take dec_gemm, larger ones fix_gemm
 constexpr int NT = 256;
 
 __device__ __forceinline__ double bf16_to_f64(uint32_t u) {
@@ -52,12 +54,30 @@ __device__ __forceinline__ double gelu64(double u) {
   return 0.5 * u * (1.0 + tanh(c * (u + ga * (u * u * u))));
 }
 
+// L2 load as a volatile asm statement: consecutive calls are issued back to back
+// (the compiler may not sink them next to their consumers), so a batch of them
+// is in flight together.
+__device__ __forceinline__ double ld_cg_batched(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// fp64 MMA m8n8k4 (row.col): c[8x8] += a[8x4] * b[4x8]; lane (g = lane/4, q = lane%4)
+// holds a[g][q], b[q][g], c[g][2q .. 2q+1]
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 // smem: As[2][KS][TM], Bs[2][KS][TN]; epilogue reuses it for hs[TM][TN+1] and w2s[TN][E]
 template <int XT, int WT>
 __global__ void __launch_bounds__(NT, 2)
 fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   extern __shared__ double sm[];
   const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
+  if (a.rows && count <= DEC_ROWS_MAX) return;  // dec_gemm's share
   const int64_t nrows = count < cap ? count : cap;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * TM;
   if (r0 >= nrows) return;
@@ -224,7 +244,7 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
 
 // one warp per flagged token: z = sum over hidden tiles (fixed order) + b2, ranks, outputs, counters
 __global__ void __launch_bounds__(256)
-fix_finish(moep_fp64_args a, int64_t cap, int ntile_h, const double* __restrict__ part, int n_counters) {
+fix_finish(moep_fp64_args a, int64_t cap, int ntile_big, const double* __restrict__ part, int n_counters) {
   extern __shared__ double zsm[];  // [8 warps][E] z values, then int ranks [8][E]
   __shared__ int scal[2 + 2 * MOEP_MAX_BOUNDS];
   const int E = a.n_experts;
@@ -235,14 +255,26 @@ fix_finish(moep_fp64_args a, int64_t cap, int ntile_h, const double* __restrict_
   if (threadIdx.x < 2 + 2 * MOEP_MAX_BOUNDS) scal[threadIdx.x] = 0;
   __syncthreads();
   const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
+  if (!a.rows || count <= DEC_ROWS_MAX) return;  // dec_finish's share (it writes the partials)
   const int64_t nrows = count < cap ? count : cap;
+  const int ntile_h = ntile_big;
   double* z = zsm + warp * E;
   int* rk = rkall + warp * E;
   for (int64_t it = static_cast<int64_t>(blockIdx.x) * 8 + warp; it < nrows; it += static_cast<int64_t>(gridDim.x) * 8) {
     const int64_t row = a.rows ? a.rows[it] : it;
     for (int e = lane; e < E; e += 32) {
+      // fixed order; loads batched so 8 are in flight together
       double s = 0.0;
-      for (int t = 0; t < ntile_h; ++t) s += part[(it * ntile_h + t) * E + e];
+      const double* pp = part + it * ntile_h * E + e;
+      int t = 0;
+      for (; t + 8 <= ntile_h; t += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_cg_batched(pp + (t + u) * E);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      for (; t < ntile_h; ++t) s += __ldcg(pp + t * E);
       z[e] = s + a.b2[e];
     }
     __syncwarp();
@@ -301,19 +333,529 @@ fix_finish(moep_fp64_args a, int64_t cap, int ntile_h, const double* __restrict_
   }
 }
 
+// Finish for the split-hidden partials (decode batches and small flagged
+// counts): one CTA per token, thread (e, g) sums tile group g of expert e,
+// groups combined in fixed order; stable ranks one expert per thread.
+constexpr int FT = 1024;  // dec_finish threads
+
+__global__ void __launch_bounds__(FT)
+dec_finish(moep_fp64_args a, int64_t cap, int ntile, const double* __restrict__ part, int n_counters) {
+  extern __shared__ double dsm[];
+  const int E = a.n_experts;
+  const int G = E >= FT ? 1 : FT / E;          // tile groups per expert
+  double* ps = dsm;                            // [G][E]
+  double* z = ps + G * E;                      // [E]
+  int* rk = reinterpret_cast<int*>(z + E);     // [E]
+  int* hist = rk + E;                          // [2E]
+  __shared__ int scal[2 + 2 * MOEP_MAX_BOUNDS];
+  __shared__ int wcnt[FT / 32];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 2 * E; i += FT) hist[i] = 0;
+  if (tid < 2 + 2 * MOEP_MAX_BOUNDS) scal[tid] = 0;
+  __syncthreads();
+  const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
+  const bool mine = !a.rows || count <= DEC_ROWS_MAX;
+  const int64_t nrows = !mine ? 0 : (count < cap ? count : cap);
+  if (!mine && !a.partials) return;
+  const int per = (ntile + G - 1) / G;
+  for (int64_t it = blockIdx.x; it < nrows; it += gridDim.x) {
+    const int64_t row = a.rows ? a.rows[it] : it;
+    // split-hidden partials are [row][E][ntile]: the tiles of one (row, e) are contiguous
+    const double* pp = part + it * E * ntile;
+    for (int q = tid; q < G * E; q += FT) {
+      const int e = q % E, g = q / E;
+      const int tb = g * per, te = (tb + per) < ntile ? (tb + per) : ntile;
+      const double* src = pp + static_cast<int64_t>(e) * ntile;
+      double sacc = 0.0;
+      int t = tb;
+      if ((ntile & 1) == 0 && (tb & 1) == 0) {
+        for (; t + 8 <= te; t += 8) {          // 4 x 16-byte loads in flight, then fixed-order adds
+          const double2* s2 = reinterpret_cast<const double2*>(src + t);
+          const double2 v0 = s2[0], v1 = s2[1], v2 = s2[2], v3 = s2[3];
+          sacc += v0.x; sacc += v0.y; sacc += v1.x; sacc += v1.y;
+          sacc += v2.x; sacc += v2.y; sacc += v3.x; sacc += v3.y;
+        }
+      }
+      for (; t < te; ++t) sacc += src[t];
+      ps[g * E + e] = sacc;
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += FT) {
+      double sacc = 0.0;
+      for (int g = 0; g < G; ++g) sacc += ps[g * E + e];
+      z[e] = sacc + a.b2[e];
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += FT) {
+      const double ze = z[e];
+      int r = 0;
+      for (int q = 0; q < E; ++q) r += key_gt(z[q], q, ze, e) ? 1 : 0;
+      rk[e] = r;
+      if (a.logits64) a.logits64[row * E + e] = ze;
+      if (a.logits32) a.logits32[row * E + e] = static_cast<float>(ze);
+    }
+    __syncthreads();
+    if (a.ids && a.m_sel > 0) {
+      if (E <= FT) {
+        // ascending ids: e is selected iff rk[e] < m; its slot = selected experts below it
+        const int lane = tid & 31, warp = tid >> 5;
+        const bool sel = tid < E && rk[tid] < a.m_sel;
+        const unsigned b = __ballot_sync(0xffffffffu, sel);
+        if (lane == 0) wcnt[warp] = __popc(b);
+        __syncthreads();
+        if (sel) {
+          int pos = __popc(b & ((1u << lane) - 1u));
+          for (int w = 0; w < warp; ++w) pos += wcnt[w];
+          a.ids[row * a.m_sel + pos] = tid;
+        }
+      } else if (tid == 0) {
+        int cnt = 0;
+        for (int e = 0; e < E && cnt < a.m_sel; ++e)
+          if (rk[e] < a.m_sel) a.ids[row * a.m_sel + cnt++] = e;
+      }
+    }
+    if (tid == 0) {
+      if (a.truth) {
+        int any0 = 0;
+        int inside[MOEP_MAX_BOUNDS] = {0, 0, 0, 0};
+        for (int j = 0; j < a.k; ++j) {
+          const int tt = a.truth[row * a.k + j];
+          const int r = rk[tt];
+          any0 |= r == 0;
+          ++hist[E + tt];
+          if (r < a.k) ++hist[tt];
+#pragma unroll
+          for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi)
+            if (mi < a.n_m && r < a.m_list[mi]) ++inside[mi];
+        }
+        scal[0] += 1;
+        scal[1] += any0;
+#pragma unroll
+        for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
+          if (mi < a.n_m) {
+            scal[2 + mi] += inside[mi] == a.k ? 1 : 0;
+            scal[2 + MOEP_MAX_BOUNDS + mi] += inside[mi];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (a.partials && mine) {
+    int* out = a.partials + static_cast<int64_t>(blockIdx.x) * n_counters;
+    for (int t = tid; t < n_counters; t += FT) {
+      int v;
+      if (t < 2) v = scal[t];
+      else if (t < 2 + a.n_m) v = scal[2 + (t - 2)];
+      else if (t < 2 + 2 * a.n_m) v = scal[2 + MOEP_MAX_BOUNDS + (t - 2 - a.n_m)];
+      else v = hist[t - 2 - 2 * a.n_m];
+      out[t] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- decode path
+// Few tokens (TT-token tiles), hidden split over CTAs of DH units so the W1
+// stream (the only sizeable traffic) is spread over every SM. K loop in chunks
+// of DKC staged as fp64 in smem, transposed ([k][t], [k][j]) so a warp's
+// operand reads are contiguous; warp w owns k = 16w .. 16w+15 of each chunk
+// with a (TPT tokens x JPT hidden) register tile; the 8 warp partials are
+// summed in fixed order, then bias + activation (predictor.py:193-240) and the
+// W2 partial of this CTA's hidden units -> part[(row * ntile + tile) * E + e].
+constexpr int DH = 16, DKC = 128;
+
+template <int XT, int WT, int TT>
+__global__ void __launch_bounds__(256)
+dec_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
+  constexpr int TPT = TT >= 32 ? 4 : 2;        // tokens per thread
+  constexpr int NTQ = TT / TPT;                // token groups per warp
+  constexpr int NHQ = 32 / NTQ;                // hidden groups per warp
+  constexpr int JPT = DH / NHQ;                // hidden units per thread
+  static_assert(NTQ * NHQ == 32 && JPT * NHQ == DH, "tile");
+  extern __shared__ double sm[];
+  double* xs = sm;                             // [2][DKC][TT]
+  double* ws = sm + 2 * DKC * TT;              // [2][DKC][DH]
+  const int d = a.d, H = a.hidden, E = a.n_experts;
+  // rows mode (fix-up): list indices [0, min(count, cap)), only when count is small
+  const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
+  if (a.rows && count > DEC_ROWS_MAX) return;
+  const int64_t n = count < cap ? count : cap;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.y) * TT;
+  if (t0 >= n) return;
+  __shared__ int64_t rowid[TT];
+  const int h0 = blockIdx.x * DH;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid < TT) rowid[tid] = (t0 + tid < n) ? (a.rows ? a.rows[t0 + tid] : t0 + tid) : -1;
+  __syncthreads();
+  const int tq = lane / NHQ, hq = lane % NHQ;
+  double acc[TPT][JPT];
+#pragma unroll
+  for (int i = 0; i < TPT; ++i)
+#pragma unroll
+    for (int j = 0; j < JPT; ++j) acc[i][j] = 0.0;
+  // staging: x chunk [TT][DKC] (TT*DKC/8 16-byte pieces), W1 chunk [DH][DKC] (256 pieces)
+  auto stage = [&](int buf, int k0) {
+    for (int q = tid; q < TT * (DKC / 8); q += 256) {
+      const int t = q % TT, kg = q / TT;
+      const int64_t row = rowid[t];
+      const int k = k0 + kg * 8;
+      double v[8];
+      if (row >= 0 && k + 8 <= d && (d % 8) == 0) {
+        if constexpr (XT == MOEP_BF16) {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.x) + row * d + k));
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = bf16_to_f64((c & 1) ? (w[c >> 1] >> 16) : (w[c >> 1] & 0xffffu));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = reinterpret_cast<const double*>(a.x)[row * d + k + c];
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = (row >= 0 && k + c < d) ? ld1<XT>(a.x, row * d + k + c) : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) xs[(buf * DKC + kg * 8 + c) * TT + t] = v[c];
+    }
+    {
+      const int j = tid % DH, kg = tid / DH;  // 16 x 16 pieces of 8
+      const int jg = h0 + j, k = k0 + kg * 8;
+      double v[8];
+      if (jg < H && k + 8 <= d && (d % 8) == 0) {
+        if constexpr (WT == MOEP_BF16) {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.w1) +
+                                                               static_cast<int64_t>(jg) * d + k));
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = bf16_to_f64((c & 1) ? (w[c >> 1] >> 16) : (w[c >> 1] & 0xffffu));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = reinterpret_cast<const double*>(a.w1)[static_cast<int64_t>(jg) * d + k + c];
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          v[c] = (jg < H && k + c < d) ? ld1<WT>(a.w1, static_cast<int64_t>(jg) * d + k + c) : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) ws[(buf * DKC + kg * 8 + c) * DH + j] = v[c];
+    }
+  };
+  const int nk = (d + DKC - 1) / DKC;
+  stage(0, 0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) stage(buf ^ 1, (kt + 1) * DKC);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int k = warp * 16 + s;
+      double av[TPT], bv[JPT];
+      const double* xp = xs + (buf * DKC + k) * TT + tq * TPT;
+      const double* wp = ws + (buf * DKC + k) * DH + hq * JPT;
+#pragma unroll
+      for (int i = 0; i < TPT; i += 2) {
+        const double2 p = *reinterpret_cast<const double2*>(xp + i);
+        av[i] = p.x; av[i + 1] = p.y;
+      }
+#pragma unroll
+      for (int j = 0; j < JPT; j += 2) {
+        const double2 p = *reinterpret_cast<const double2*>(wp + j);
+        bv[j] = p.x; bv[j + 1] = p.y;
+      }
+#pragma unroll
+      for (int i = 0; i < TPT; ++i)
+#pragma unroll
+        for (int j = 0; j < JPT; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  // fixed-order reduction over the 8 warps' K slices
+  double* red = sm;                            // [8][TT][DH]
+#pragma unroll
+  for (int i = 0; i < TPT; ++i)
+#pragma unroll
+    for (int j = 0; j < JPT; ++j) red[(warp * TT + tq * TPT + i) * DH + hq * JPT + j] = acc[i][j];
+  __syncthreads();
+  double* hs = sm + 8 * TT * DH;               // [TT][DH]
+  for (int o = tid; o < TT * DH; o += 256) {
+    const int t = o / DH, j = o % DH, jg = h0 + j;
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[(w * TT + t) * DH + j];
+    double hv = 0.0;
+    if (jg < H && rowid[t] >= 0) {
+      const double av = s + a.b1[jg];
+      if (a.a_out) a.a_out[rowid[t] * H + jg] = av;
+      if (a.arch == 2) {
+        hv = av * sigmoid64(av);
+      } else {
+        const double inv_std = 1.0 / sqrt(a.bn_var[jg] + a.bn_eps);
+        hv = gelu64(a.bn_scale[jg] * ((av - a.bn_mean[jg]) * inv_std) + a.bn_shift[jg]);
+      }
+    }
+    hs[o] = hv;
+  }
+  __syncthreads();
+  const int jn = (H - h0) < DH ? (H - h0) : DH;
+  for (int o = tid; o < TT * E; o += 256) {
+    const int t = o / E, e = o - t * E;
+    if (rowid[t] < 0) continue;
+    double s = 0.0;
+    for (int j = 0; j < jn; ++j) s = fma(hs[t * DH + j], ld1<WT>(a.w2t, static_cast<int64_t>(h0 + j) * E + e), s);
+    part[((t0 + t) * E + e) * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// Bulk-copy variant for bf16 x / W1 with d % DKC == 0 (the serving case): the
+// CTA's W1 slice [DH][d] and its token rows [TT][d] are fetched by the TMA
+// engine with one 1-D bulk copy per (row, K chunk), all issued up front on
+// per-chunk mbarriers, so the HBM latency is paid once instead of per chunk.
+// Warp w converts and consumes only K columns 16w..16w+15 of each chunk, so
+// the K loop needs no CTA-wide barrier.
+template <int TT>
+__global__ void __launch_bounds__(256)
+dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
+  static_assert(TT % 8 == 0 && DH == 16, "tile");
+  extern __shared__ __align__(128) uint8_t smb[];
+  const int d = a.d, H = a.hidden, E = a.n_experts;
+  const int rp = d + 8;                        // raw bf16 row pitch (16 B pad: 4-bank shift per row)
+  const int nk = d / DKC;
+  uint16_t* wraw = reinterpret_cast<uint16_t*>(smb);            // [DH][rp]
+  uint16_t* xraw = wraw + DH * rp;                               // [TT][rp]
+  size_t rawb = sizeof(uint16_t) * (DH + TT) * rp;                // same layout as dec_bulk_smem
+  if (rawb < sizeof(double) * 9 * TT * DH) rawb = sizeof(double) * 9 * TT * DH;
+  rawb = (rawb + 15) & ~static_cast<size_t>(15);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smb + rawb);        // [nseg]
+  uint16_t* w2smem = (E % 8 == 0) ? reinterpret_cast<uint16_t*>(bars + 4) : nullptr;  // [DH][E]
+  const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
+  if (a.rows && count > DEC_ROWS_MAX) return;
+  const int64_t n = count < cap ? count : cap;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.y) * TT;
+  if (t0 >= n) return;
+  __shared__ int64_t rowid[TT];
+  const int h0 = blockIdx.x * DH;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nv = static_cast<int>((n - t0) < TT ? (n - t0) : TT);
+  const int hv = (H - h0) < DH ? (H - h0) : DH;
+  if (tid < TT) rowid[tid] = tid < nv ? (a.rows ? a.rows[t0 + tid] : t0 + tid) : -1;
+  // K is fetched in NSEG segments (one bulk copy per row and segment, one
+  // mbarrier per segment): few large TMA requests, and the first segment's
+  // compute overlaps the rest of the transfer
+  const int nseg = (nk % 4 == 0) ? 4 : ((nk % 2 == 0) ? 2 : 1);
+  const int cps = nk / nseg;                   // chunks per segment
+  const int segk = cps * DKC;
+  if (tid == 0) {
+    for (int c = 0; c < nseg; ++c) mbar_init(&bars[c], 1);
+    fence_barrier_init();
+    for (int c = 0; c < nseg; ++c)
+      mbar_arrive_expect_tx(&bars[c], static_cast<uint32_t>((nv + hv) * segk * 2 + (c == 0 && w2smem ? hv * E * 2 : 0)));
+    if (w2smem)
+      bulk_g2s(w2smem, reinterpret_cast<const uint16_t*>(a.w2t) + static_cast<int64_t>(h0) * E, hv * E * 2, &bars[0]);
+  }
+  __syncthreads();
+  {
+    const int R = nv + hv;
+    const uint16_t* xg = reinterpret_cast<const uint16_t*>(a.x);
+    const uint16_t* wg = reinterpret_cast<const uint16_t*>(a.w1);
+    for (int q = tid; q < R * nseg; q += 256) {
+      const int r = q % R, c = q / R;
+      if (r < nv)
+        bulk_g2s(xraw + r * rp + c * segk, xg + rowid[r] * d + c * segk, segk * 2, &bars[c]);
+      else
+        bulk_g2s(wraw + (r - nv) * rp + c * segk, wg + static_cast<int64_t>(h0 + r - nv) * d + c * segk, segk * 2,
+                 &bars[c]);
+    }
+  }
+  // fp64 tensor-core MMA (m8n8k4): A = x [8 tokens x 4 k], B = W1^T [4 k x 8
+  // hidden], operands converted straight from the raw bf16 rows (lane (g, q)
+  // reads row g, column q: rows are 4 banks apart, conflict-free)
+  constexpr int MT = TT / 8;
+  const int g = lane >> 2, q4 = lane & 3;
+  double acc[MT][2][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  const int kw = warp * 16;                    // this warp's 16 columns of every chunk
+  for (int c = 0; c < nk; ++c) {
+    if (c % cps == 0) mbar_wait(&bars[c / cps], 0);
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4) {
+      const int k = c * DKC + kw + s4 * 4 + q4;
+      double av[MT], bv[2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int t = g + 8 * mt;
+        av[mt] = t < nv ? static_cast<double>(__uint_as_float(static_cast<uint32_t>(xraw[t * rp + k]) << 16)) : 0.0;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int jj = g + 8 * nt;
+        bv[nt] = jj < hv ? static_cast<double>(__uint_as_float(static_cast<uint32_t>(wraw[jj * rp + k]) << 16)) : 0.0;
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma884(acc[mt][nt], av[mt], bv[nt]);
+    }
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < nseg; ++c) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[c])));
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(smb);  // [8][TT][DH], reuses the raw region (sized for it)
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+        red[(warp * TT + g + 8 * mt) * DH + 8 * nt + 2 * q4 + hh] = acc[mt][nt][hh];
+  __syncthreads();
+  double* hs = red + 8 * TT * DH;              // [TT][DH]
+  for (int o = tid; o < TT * DH; o += 256) {
+    const int t = o / DH, j = o % DH, jg = h0 + j;
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sum += red[(w * TT + t) * DH + j];
+    double hval = 0.0;
+    if (jg < H && rowid[t] >= 0) {
+      const double av = sum + a.b1[jg];
+      if (a.a_out) a.a_out[rowid[t] * H + jg] = av;
+      if (a.arch == 2) {
+        hval = av * sigmoid64(av);
+      } else {
+        const double inv_std = 1.0 / sqrt(a.bn_var[jg] + a.bn_eps);
+        hval = gelu64(a.bn_scale[jg] * ((av - a.bn_mean[jg]) * inv_std) + a.bn_shift[jg]);
+      }
+    }
+    hs[o] = hval;
+  }
+  __syncthreads();
+  // W2 partial: thread = expert e; its DH W2^T values (bulk-copied into smem
+  // with the first K segment when E % 8 == 0) are reused for every token
+  const uint16_t* w2t = reinterpret_cast<const uint16_t*>(a.w2t);
+  const uint16_t* w2s = w2smem ? w2smem : w2t + static_cast<int64_t>(h0) * E;
+  for (int e = tid; e < E; e += 256) {
+    double wv[DH];
+#pragma unroll
+    for (int j = 0; j < DH; ++j) {
+      const int jj = j < hv ? j : hv - 1;       // clamped: unconditional loads stay batched
+      const double w = static_cast<double>(__uint_as_float(static_cast<uint32_t>(w2s[jj * E + e]) << 16));
+      wv[j] = j < hv ? w : 0.0;
+    }
+    for (int t = 0; t < nv; ++t) {
+      double sum = 0.0;
+#pragma unroll
+      for (int j = 0; j < DH; ++j) sum = fma(hs[t * DH + j], wv[j], sum);
+      part[((t0 + t) * E + e) * gridDim.x + blockIdx.x] = sum;
+    }
+  }
+}
+
+template <int TT>
+static size_t dec_bulk_smem(int d, int E) {
+  // raw rows + barriers + W2^T slice; the epilogue's warp partials + hidden tile
+  // (9 * TT * DH doubles) reuse the raw rows and must not reach the W2 slice
+  size_t raw = sizeof(uint16_t) * (DH + TT) * (d + 8);
+  const size_t red = sizeof(double) * 9 * TT * DH;
+  if (raw < red) raw = red;
+  raw = (raw + 15) & ~static_cast<size_t>(15);
+  return raw + sizeof(uint64_t) * 4 + sizeof(uint16_t) * DH * E;
+}
+
 }  // namespace k2b
 }  // namespace moep
+
+namespace moep {
+namespace k2b {
+// dec_gemm over list indices [0, cap): 8-token tiles for cap <= 8, else 32
+static int launch_dec(const moep_fp64_args* a, int64_t cap, double* scratch, cudaStream_t st) {
+  const int ntile = (a->hidden + DH - 1) / DH;
+  const bool xb = a->x_dtype == MOEP_BF16, wb = a->w_dtype == MOEP_BF16;
+  // bulk-copy kernel: bf16 x and W1, d a multiple of DKC, 16-byte aligned rows
+  const bool bulk_ok = xb && wb && (a->d % DKC) == 0 && (reinterpret_cast<uintptr_t>(a->x) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(a->w1) & 15) == 0;
+  auto gob = [&](auto kern, int tt, size_t smem) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+      return MOEP_ELAUNCH;
+    dim3 grid(static_cast<unsigned>(ntile), static_cast<unsigned>((cap + tt - 1) / tt));
+    kern<<<grid, 256, smem, st>>>(*a, cap, scratch);
+    return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+  };
+  constexpr size_t kSmemMax = 227 * 1024;
+  if (bulk_ok && cap > 8 && dec_bulk_smem<16>(a->d, a->n_experts) <= kSmemMax)
+    return gob(dec_gemm_bulk<16>, 16, dec_bulk_smem<16>(a->d, a->n_experts));
+  if (bulk_ok && cap <= 8 && dec_bulk_smem<8>(a->d, a->n_experts) <= kSmemMax)
+    return gob(dec_gemm_bulk<8>, 8, dec_bulk_smem<8>(a->d, a->n_experts));
+  auto go = [&](auto kern, int tt) {
+    const size_t smem = sizeof(double) * 2 * DKC * (tt + DH);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+      return MOEP_ELAUNCH;
+    dim3 grid(static_cast<unsigned>(ntile), static_cast<unsigned>((cap + tt - 1) / tt));
+    kern<<<grid, 256, smem, st>>>(*a, cap, scratch);
+    return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+  };
+  if (cap <= 8) {
+    if (xb && wb) return go(dec_gemm<MOEP_BF16, MOEP_BF16, 8>, 8);
+    if (xb) return go(dec_gemm<MOEP_BF16, MOEP_F64, 8>, 8);
+    if (wb) return go(dec_gemm<MOEP_F64, MOEP_BF16, 8>, 8);
+    return go(dec_gemm<MOEP_F64, MOEP_F64, 8>, 8);
+  }
+  if (xb && wb) return go(dec_gemm<MOEP_BF16, MOEP_BF16, 32>, 32);
+  if (xb) return go(dec_gemm<MOEP_BF16, MOEP_F64, 32>, 32);
+  if (wb) return go(dec_gemm<MOEP_F64, MOEP_BF16, 32>, 32);
+  return go(dec_gemm<MOEP_F64, MOEP_F64, 32>, 32);
+}
+
+// finish kernels: dec_finish for split-hidden partials (all-rows mode, or a
+// flagged count <= DEC_ROWS_MAX), fix_finish for fix_gemm partials (larger
+// counts); in rows mode both are launched and each exits unless the device
+// count is its share. With evaluation partials every one of the num_sms
+// partial rows is written by exactly one of them.
+static int launch_finish(const moep_fp64_args* a, int64_t cap, double* scratch, cudaStream_t st, bool big) {
+  const int E = a->n_experts;
+  const int ncnt = a->truth ? moep_n_counters(a->n_m, E) : 0;
+  const int nsm = moep_num_sms();
+  const int G = E >= FT ? 1 : FT / E;
+  const size_t dsmem = sizeof(double) * (G * E + E) + sizeof(int) * (3 * E);
+  const int64_t dcap = (a->rows && cap > DEC_ROWS_MAX) ? DEC_ROWS_MAX : cap;
+  const int dgrid = a->partials ? nsm : static_cast<int>(dcap < nsm ? dcap : nsm);
+  dec_finish<<<dgrid, FT, dsmem, st>>>(*a, cap, (a->hidden + DH - 1) / DH, scratch, ncnt);
+  if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
+  if (!big) return MOEP_OK;
+  const size_t fsmem = sizeof(double) * 8 * E + sizeof(int) * (8 * E + 2 * E);
+  const int64_t nblk = (cap + 7) / 8;
+  const int grid = a->partials ? nsm : static_cast<int>(nblk < nsm ? nblk : nsm);
+  fix_finish<<<grid, 256, fsmem, st>>>(*a, cap, (a->hidden + TN - 1) / TN, scratch, ncnt);
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+}  // namespace k2b
+}  // namespace moep
+
+extern "C" int moep_decode_fp64(const moep_fp64_args* a, double* scratch, void* stream) {
+  using namespace moep::k2b;
+  if (!a || a->n_tokens <= 0 || a->d <= 0 || a->hidden <= 0 || a->n_experts <= 0) return MOEP_ESHAPE;
+  if (!a->w2t || !scratch || a->rows || a->row_begin != 0) return MOEP_EARG;
+  if (a->arch != 1 && a->arch != 2) return MOEP_EARG;
+  if (a->truth && (a->k < 1 || a->k > 16 || a->n_m < 0 || a->n_m > MOEP_MAX_BOUNDS)) return MOEP_EARG;
+  if (a->m_sel < 0 || a->m_sel > a->n_experts) return MOEP_EARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int rc = launch_dec(a, a->n_tokens, scratch, st);
+  if (rc != MOEP_OK) return rc;
+  return launch_finish(a, a->n_tokens, scratch, st, false);
+}
 
 extern "C" int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t cap, int32_t* partials2,
                                void* stream) {
   using namespace moep::k2b;
   if (!a || a->n_tokens <= 0 || a->d <= 0 || a->hidden <= 0 || a->n_experts <= 0) return MOEP_ESHAPE;
-  if (!a->w2t || !scratch || cap <= 0) return MOEP_EARG;
+  if (!a->w2t || !scratch || cap <= 0 || !a->rows || !a->row_count) return MOEP_EARG;
   if (a->arch != 1 && a->arch != 2) return MOEP_EARG;
   if (a->truth && (a->k < 1 || a->k > 16 || a->n_m < 0 || a->n_m > MOEP_MAX_BOUNDS)) return MOEP_EARG;
   if (a->m_sel < 0 || a->m_sel > a->n_experts) return MOEP_EARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int E = a->n_experts;
   const int ntile_h = (a->hidden + TN - 1) / TN;
   const size_t smem_main = sizeof(double) * 2 * KS * (TM + TN);
   const size_t smem_epi = sizeof(double) * (TM * (TN + 1));
@@ -333,10 +875,11 @@ extern "C" int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t
   else if (wb) rc = go(fix_gemm<MOEP_F64, MOEP_BF16>);
   else rc = go(fix_gemm<MOEP_F64, MOEP_F64>);
   if (rc != MOEP_OK) return rc;
-  const int ncnt = a->truth ? moep_n_counters(a->n_m, E) : 0;
-  const size_t fsmem = sizeof(double) * 8 * E + sizeof(int) * (8 * E + 2 * E);
-  fix_finish<<<moep_num_sms(), 256, fsmem, st>>>(*a, cap, ntile_h, scratch, ncnt);
-  if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
+  // small flagged counts (decided on the device): the split-hidden kernel
+  rc = launch_dec(a, cap < DEC_ROWS_MAX ? cap : DEC_ROWS_MAX, scratch, st);
+  if (rc != MOEP_OK) return rc;
+  rc = launch_finish(a, cap, scratch, st, true);  // the device count picks the finish kernel
+  if (rc != MOEP_OK) return rc;
   // rows beyond the scratch capacity: the per-group kernel, starting at row `cap`
   moep_fp64_args b = *a;
   b.row_begin = cap;

@@ -26,6 +26,7 @@ K1_MAX_SEL = 15       # K1 keeps 16 sorted positions per token
 K1_MAX_EXPERTS = 128  # TMEM budget of the single-CTA kernel
 TAU_ABS = 1e-7
 TAU_REL = 2e-6
+DECODE_MAX_TOKENS = 64  # batches up to this size take the split-hidden exact fp64 decode kernel
 
 
 def _require_cuda(device) -> torch.device:
@@ -138,6 +139,8 @@ class DevicePredictor:
             code = MOEP_F64
         x = x.contiguous()
         n = x.shape[0]
+        if x.dtype == torch.bfloat16 and not check_finite:
+            return x, x, True  # no host synchronisation (serving path)
         if x.dtype == torch.bfloat16:
             xb = x
             status = torch.zeros(2, dtype=torch.int32, device=self.device)
@@ -170,6 +173,27 @@ class DevicePredictor:
                                     float(eps), ptr(out), ptr(status), _stream(self.device)),
               "moep_input_norm")
         return out
+
+    def _decode_input(self, x: torch.Tensor, validate: bool):
+        """Decode path input: bf16 or fp64 on device (no cast kernel, no host
+        sync unless validate). Non-finite input raises ConfigurationError
+        (predictor.py:188-189) when validate is set."""
+        x = x.to(self.device)
+        if x.dim() != 2 or x.shape[1] != self.d:
+            raise ConfigurationError(f"input shape {tuple(x.shape)} incompatible with d={self.d}")
+        if x.dtype not in (torch.bfloat16, torch.float64):
+            x = x.to(torch.float64)
+        x = x.contiguous()
+        if validate and not bool(torch.isfinite(x).all()):
+            raise ConfigurationError("input must be finite")
+        return x, (MOEP_BF16 if x.dtype == torch.bfloat16 else MOEP_F64)
+
+    def _decode(self, x, code, **kw):
+        """moep_decode_fp64: exact fp64 logits / ids / counters for all rows."""
+        a = self._fp64_args(x, code, **kw)
+        scratch = torch.empty(x.shape[0] * ((self.hidden + 15) // 16) * self.E, dtype=torch.float64,
+                              device=self.device)
+        check(lib().moep_decode_fp64(a, ptr(scratch), _stream(self.device)), "moep_decode_fp64")
 
     # --------------------------------------------------------------- kernels
     def _fp64_args(self, x, x_code, rows=None, row_count=None, m_sel=0, ids=None, logits64=None,
@@ -224,6 +248,7 @@ class DevicePredictor:
                 and self.d % 8 == 0 and self.hidden % 8 == 0
                 and all(p <= K1_MAX_SEL or p >= self.E for p in positions))
 
+    decode_max_tokens = DECODE_MAX_TOKENS  # 0 forces the tensor-core path for every batch
     fixup_capacity = None  # rows handled by the GEMM fix-up per call (None: max(2048, N/128))
 
     def _fixup(self, a, n, partials2=None):
@@ -231,15 +256,20 @@ class DevicePredictor:
         cap = self.fixup_capacity or max(2048, n // 128)
         if cap > n:
             cap = n
-        ntile_h = (self.hidden + 127) // 128
-        scratch = torch.empty(cap * ntile_h * self.E, dtype=torch.float64, device=self.device)
+        size = max(cap * ((self.hidden + 127) // 128), min(cap, 256) * ((self.hidden + 15) // 16)) * self.E
+        scratch = torch.empty(size, dtype=torch.float64, device=self.device)
         check(lib().moep_fixup_fp64(a, ptr(scratch), cap, ptr(partials2), _stream(self.device)),
               "moep_fixup_fp64")
 
     # ------------------------------------------------------------------ API
-    def logits(self, x: torch.Tensor, return_flags=False):
+    def logits(self, x: torch.Tensor, return_flags=False, validate=True):
         """fp64 logits [N, E] (predict_logits)."""
-        x, xb, exact = self.prepare(x)
+        if 0 < x.shape[0] <= self.decode_max_tokens:
+            xs, code = self._decode_input(x, validate)
+            out64 = torch.empty((xs.shape[0], self.E), dtype=torch.float64, device=self.device)
+            self._decode(xs, code, logits64=out64)
+            return (out64, None) if return_flags else out64
+        x, xb, exact = self.prepare(x, check_finite=validate)
         n = x.shape[0]
         out64 = torch.empty((n, self.E), dtype=torch.float64, device=self.device)
         if self.k1_usable(exact):
@@ -257,11 +287,20 @@ class DevicePredictor:
             flags = None
         return (out64, flags) if return_flags else out64
 
-    def topk(self, x: torch.Tensor, m: int, return_flags=False):
-        """Ascending top-m expert ids [N, m] (predict_topk_batch)."""
+    def topk(self, x: torch.Tensor, m: int, return_flags=False, validate=True):
+        """Ascending top-m expert ids [N, m] (predict_topk_batch).
+
+        Decode batches (N <= DECODE_MAX_TOKENS) run the exact fp64 decode
+        kernel; with validate=False that path does no host synchronisation
+        (serving: the ids feed the prefetch plan on the device)."""
         if not 1 <= m <= self.E:
             raise ValueError(f"m={m} out of range for {self.E} experts")
-        x, xb, exact = self.prepare(x)
+        if 0 < x.shape[0] <= self.decode_max_tokens:
+            xs, code = self._decode_input(x, validate)
+            ids = torch.empty((xs.shape[0], m), dtype=torch.int32, device=self.device)
+            self._decode(xs, code, m_sel=m, ids=ids)
+            return (ids, None) if return_flags else ids
+        x, xb, exact = self.prepare(x, check_finite=validate)
         n = x.shape[0]
         ids = torch.empty((n, m), dtype=torch.int32, device=self.device)
         flags = None
@@ -287,13 +326,23 @@ class DevicePredictor:
         m_values = sorted(set(int(m) for m in m_values))
         if k not in m_values:
             m_values.insert(0, k)
+        truth = truth.to(device=self.device, dtype=torch.int32).contiguous()
+        ncnt = 2 + 2 * len(m_values) + 2 * self.E
+        if prepared is None and 0 < x.shape[0] <= self.decode_max_tokens and len(m_values) <= _lib.MAX_BOUNDS \
+                and k <= 16:
+            xs, code = self._decode_input(x, True)
+            partials = torch.empty((self.n_sms, ncnt), dtype=torch.int32, device=self.device)
+            counters = torch.empty(ncnt, dtype=torch.int64, device=self.device)
+            ids = torch.empty((xs.shape[0], ids_m), dtype=torch.int32, device=self.device) if ids_m else None
+            self._decode(xs, code, m_sel=ids_m, ids=ids, truth=truth, k=k, m_values=m_values, partials=partials)
+            check(lib().moep_counters_reduce(ptr(partials), self.n_sms, ncnt, ptr(counters),
+                                             _stream(self.device)), "moep_counters_reduce")
+            return counters, torch.zeros(1, dtype=torch.int32, device=self.device), ids
         if prepared is None:
             x, xb, exact = self.prepare(x)
         else:
             x, xb, exact = prepared
         n = x.shape[0]
-        truth = truth.to(device=self.device, dtype=torch.int32).contiguous()
-        ncnt = 2 + 2 * len(m_values) + 2 * self.E
         # partial rows: [K1 | fix-up finish | fix-up overflow], one per SM each
         partials = torch.empty((3 * self.n_sms, ncnt), dtype=torch.int32, device=self.device)
         counters = torch.empty(ncnt, dtype=torch.int64, device=self.device)
