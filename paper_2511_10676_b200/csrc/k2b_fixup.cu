@@ -66,12 +66,15 @@ __device__ __forceinline__ double ld_cg_batched(const double* p) {
 // fp64 MMA m8n8k4 (row.col): c[8x8] += a[8x4] * b[4x8]; lane (g = lane/4, q = lane%4)
 // holds a[g][q], b[q][g], c[g][2q .. 2q+1]
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
 
-// smem: As[2][KS][TM], Bs[2][KS][TN]; epilogue reuses it for hs[TM][TN+1] and w2s[TN][E]
+// smem: As[2][KS][AP], Bs[2][KS][BP] (k-major, padded pitches: conflict-free
+// DMMA fragment reads); the epilogue reuses it for hs[TM][TN+1].
+constexpr int AP = TM + 4, BP = TN + 4;
+
 template <int XT, int WT>
 __global__ void __launch_bounds__(NT, 2)
 fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
@@ -84,8 +87,8 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   const int d = a.d, H = a.hidden, E = a.n_experts;
   const int h0 = blockIdx.y * TN;
   const int ntile_h = gridDim.y;
-  double* As = sm;                    // [2][KS][TM]
-  double* Bs = sm + 2 * KS * TM;      // [2][KS][TN]
+  double* As = sm;                    // [2][KS][AP]
+  double* Bs = sm + 2 * KS * AP;      // [2][KS][BP]
   __shared__ int64_t rowid[TM];
   const int tid = threadIdx.x;
   if (tid < TM) {
@@ -93,44 +96,33 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
     rowid[tid] = it < nrows ? (a.rows ? a.rows[it] : it) : -1;
   }
   __syncthreads();
-  const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads: ty -> 4 tokens, tx -> 8 hidden
-  double acc[4][8];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
 
   // global -> smem loaders. A tile [KS][TM]: thread = (row r = tid % 64, k-quarter
   // tid / 64) reads 4 consecutive k of its row; B tile [KS][TN]: thread = (hidden
   // row n = tid % 128, k-half tid / 128) reads 8 consecutive k (one 16-byte bf16
-  // load). Consecutive lanes write consecutive smem columns: conflict-free.
-  // Global loads of tile kt+1 are issued into registers before the MMA-free
-  // compute of tile kt and stored (converted to fp64) after it, so their L2
-  // latency overlaps the DFMA work. Vector loads when d % 8 == 0.
+  // load). Global loads of tile kt+1 are issued into registers before the
+  // compute of tile kt and stored (converted to fp64) after it.
   const int ar = tid & (TM - 1), akq = tid / TM;   // A: row, k-quarter
   const int bn = tid & (TN - 1), bkh = tid / TN;   // B: hidden row, k-half
   const int64_t arow = rowid[ar];
   const int bj = h0 + bn;
   const bool vec = (d % 8) == 0;
-  // staging registers: raw bf16 words (converted at stash time) or fp64 values
   uint32_t ua[2], ub[4];
   double ra[(XT == MOEP_BF16) ? 1 : 4], rb[(WT == MOEP_BF16) ? 1 : 8];
-  bool a_ok, b_ok, a_vec, b_vec;
+  bool a_vec, b_vec;
   int ka_s, kb_s;
   auto fetch = [&](int k0) {
     const int ka = k0 + akq * 4, kb = k0 + bkh * 8;
     ka_s = ka; kb_s = kb;
-    a_ok = arow >= 0 && ka < d;
-    b_ok = bj < H && kb < d;
-    a_vec = vec && a_ok;
-    b_vec = vec && b_ok;
+    a_vec = vec && arow >= 0 && ka < d;
+    b_vec = vec && bj < H && kb < d;
     if (a_vec) {
       if constexpr (XT == MOEP_BF16) {
         const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.x) + arow * d + ka));
         ua[0] = u.x; ua[1] = u.y;
       } else {
-        const double2* s = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(a.x) + arow * d + ka);
-        const double2 p0 = __ldg(s), p1 = __ldg(s + 1);
+        const double2* s2 = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(a.x) + arow * d + ka);
+        const double2 p0 = __ldg(s2), p1 = __ldg(s2 + 1);
         ra[0] = p0.x; ra[1] = p0.y; ra[2] = p1.x; ra[3] = p1.y;
       }
     }
@@ -140,10 +132,10 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
                                                             static_cast<int64_t>(bj) * d + kb));
         ub[0] = u.x; ub[1] = u.y; ub[2] = u.z; ub[3] = u.w;
       } else {
-        const double2* s = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(a.w1) +
-                                                            static_cast<int64_t>(bj) * d + kb);
+        const double2* s2 = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(a.w1) +
+                                                             static_cast<int64_t>(bj) * d + kb);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) { const double2 v = __ldg(s + c); rb[2 * c] = v.x; rb[2 * c + 1] = v.y; }
+        for (int c = 0; c < 4; ++c) { const double2 v = __ldg(s2 + c); rb[2 * c] = v.x; rb[2 * c + 1] = v.y; }
       }
     }
   };
@@ -157,7 +149,7 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
       } else {
         v = (arow >= 0 && ka_s + c < d) ? ld1<XT>(a.x, arow * d + ka_s + c) : 0.0;
       }
-      As[(buf * KS + akq * 4 + c) * TM + ar] = v;
+      As[(buf * KS + akq * 4 + c) * AP + ar] = v;
     }
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -168,9 +160,19 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
       } else {
         v = (bj < H && kb_s + c < d) ? ld1<WT>(a.w1, static_cast<int64_t>(bj) * d + kb_s + c) : 0.0;
       }
-      Bs[(buf * KS + bkh * 8 + c) * TN + bn] = v;
+      Bs[(buf * KS + bkh * 8 + c) * BP + bn] = v;
     }
   };
+  // fp64 tensor-core MMA: warp (wm, wn) owns a 32 x 32 tile = 4 x 4 m8n8 tiles;
+  // lane (g, q) holds A[m + g][k + q], B[k + q][n + g], C[m + g][n + 2q .. +1]
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int g = lane >> 2, q4 = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int nk = (d + KS - 1) / KS;
   fetch(0);
   stash(0);
@@ -179,66 +181,94 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
     const int buf = kt & 1;
     if (kt + 1 < nk) fetch((kt + 1) * KS);
 #pragma unroll
-    for (int kk = 0; kk < KS; ++kk) {
-      double av[4], bv[8];
-      const double2* ap = reinterpret_cast<const double2*>(As + (buf * KS + kk) * TM + ty * 4);
-      const double2 a01 = ap[0], a23 = ap[1];
-      av[0] = a01.x; av[1] = a01.y; av[2] = a23.x; av[3] = a23.y;
-      // thread tx owns hidden columns {jj*32 + 2*tx, jj*32 + 2*tx + 1 : jj < 4}:
-      // each double2 load spans 16 consecutive lanes x 16 B -> no bank conflicts
-      const double* brow = Bs + (buf * KS + kk) * TN + tx * 2;
+    for (int k4 = 0; k4 < KS; k4 += 4) {
+      double av[4], bv[4];
+      const double* ap = As + (buf * KS + k4 + q4) * AP + wm * 32 + g;
+      const double* bp = Bs + (buf * KS + k4 + q4) * BP + wn * 32 + g;
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const double2 b = *reinterpret_cast<const double2*>(brow + jj * 32);
-        bv[2 * jj] = b.x;
-        bv[2 * jj + 1] = b.y;
-      }
+      for (int i = 0; i < 4; ++i) av[i] = ap[8 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = bp[8 * j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], av[i], bv[j]);
     }
     if (kt + 1 < nk) stash(buf ^ 1);
     __syncthreads();
   }
-  // ---- epilogue: bias + activation -> hs [TM][TN+1]; W2^T read from L2
+  // ---- epilogue: bias + activation -> hs [TM][TN+1]
   double* hs = sm;                               // TM * (TN + 1)
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int jl = (j >> 1) * 32 + tx * 2 + (j & 1), jg = h0 + jl;
-    double b1 = 0.0, inv_std = 0.0, mean = 0.0, sc = 0.0, sh = 0.0;
-    const bool ok = jg < H;
-    if (ok) {
-      b1 = a.b1[jg];
-      if (a.arch == 1) {
-        inv_std = 1.0 / sqrt(a.bn_var[jg] + a.bn_eps);
-        mean = a.bn_mean[jg]; sc = a.bn_scale[jg]; sh = a.bn_shift[jg];
-      }
-    }
+  for (int j = 0; j < 4; ++j) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = ty * 4 + i;
-      double hv = 0.0;
+    for (int hh = 0; hh < 2; ++hh) {
+      const int jl = wn * 32 + 8 * j + 2 * q4 + hh, jg = h0 + jl;
+      double b1 = 0.0, inv_std = 0.0, mean = 0.0, sc = 0.0, sh = 0.0;
+      const bool ok = jg < H;
       if (ok) {
-        const double av = acc[i][j] + b1;
-        if (a.a_out && rowid[r] >= 0) a.a_out[rowid[r] * H + jg] = av;
-        if (a.arch == 2) hv = av * sigmoid64(av);
-        else hv = gelu64(sc * ((av - mean) * inv_std) + sh);
+        b1 = a.b1[jg];
+        if (a.arch == 1) {
+          inv_std = 1.0 / sqrt(a.bn_var[jg] + a.bn_eps);
+          mean = a.bn_mean[jg]; sc = a.bn_scale[jg]; sh = a.bn_shift[jg];
+        }
       }
-      hs[r * (TN + 1) + jl] = hv;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = wm * 32 + 8 * i + g;
+        double hv = 0.0;
+        if (ok) {
+          const double av = acc[i][j][hh] + b1;
+          if (a.a_out && rowid[r] >= 0) a.a_out[rowid[r] * H + jg] = av;
+          if (a.arch == 2) hv = av * sigmoid64(av);
+          else hv = gelu64(sc * ((av - mean) * inv_std) + sh);
+        }
+        hs[r * (TN + 1) + jl] = hv;
+      }
     }
   }
   __syncthreads();
-  // partial z for this hidden tile: thread owns (row, expert) pairs, fixed j order;
-  // consecutive threads read consecutive experts of a W2^T row (coalesced).
+  // partial z for this hidden tile. E <= 256: thread = (expert e, row group);
+  // each W2^T value is loaded once per thread (batches of 8) and applied to 16
+  // rows; per output the sum runs over j in fixed order.
   const int jn = (H - h0) < TN ? (H - h0) : TN;
-  for (int o = tid; o < TM * E; o += NT) {
-    const int r = o / E, e = o - r * E;
-    if (rowid[r] < 0) continue;
-    double s = 0.0;
-    const double* hr = hs + r * (TN + 1);
-    for (int jl = 0; jl < jn; ++jl) s = fma(hr[jl], ld1<WT>(a.w2t, static_cast<int64_t>(h0 + jl) * E + e), s);
-    part[((r0 + r) * ntile_h + blockIdx.y) * E + e] = s;
+  if (E <= NT) {
+    const int e = tid % E, ngr = NT / E, rg = tid / E;
+    if (rg < ngr) {
+      for (int rb = rg * 16; rb < TM; rb += ngr * 16) {
+        double sacc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sacc[i] = 0.0;
+        for (int j0 = 0; j0 < jn; j0 += 8) {
+          double w[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int jj = (j0 + u < jn) ? (j0 + u) : (jn - 1);
+            const double wv = ld1<WT>(a.w2t, static_cast<int64_t>(h0 + jj) * E + e);
+            w[u] = (j0 + u < jn) ? wv : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (j0 + u < jn) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) sacc[i] = fma(hs[(rb + i) * (TN + 1) + j0 + u], w[u], sacc[i]);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (rowid[rb + i] >= 0) part[((r0 + rb + i) * ntile_h + blockIdx.y) * E + e] = sacc[i];
+      }
+    }
+  } else {
+    for (int o = tid; o < TM * E; o += NT) {
+      const int r = o / E, e = o - r * E;
+      if (rowid[r] < 0) continue;
+      double sacc = 0.0;
+      const double* hr = hs + r * (TN + 1);
+      for (int jl = 0; jl < jn; ++jl) sacc = fma(hr[jl], ld1<WT>(a.w2t, static_cast<int64_t>(h0 + jl) * E + e), sacc);
+      part[((r0 + r) * ntile_h + blockIdx.y) * E + e] = sacc;
+    }
   }
 }
 
@@ -857,7 +887,7 @@ extern "C" int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t
   if (a->m_sel < 0 || a->m_sel > a->n_experts) return MOEP_EARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int ntile_h = (a->hidden + TN - 1) / TN;
-  const size_t smem_main = sizeof(double) * 2 * KS * (TM + TN);
+  const size_t smem_main = sizeof(double) * 2 * KS * (AP + BP);
   const size_t smem_epi = sizeof(double) * (TM * (TN + 1));
   const size_t smem = smem_main > smem_epi ? smem_main : smem_epi;
   if (smem > 200 * 1024) return MOEP_EUNSUPPORTED;
