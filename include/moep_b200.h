@@ -78,9 +78,18 @@ typedef struct {
   int32_t m_list[MOEP_MAX_BOUNDS];
   int32_t* partials;          /* [moep_num_sms(), n_counters] int32 */
   float* a_out;               /* [N, hidden] fp32 pre-activation W1.x + b1 (training), or NULL */
+  float* split_scratch;       /* hidden-split partial logits for small N (see below), or NULL */
+  int64_t split_scratch_floats;
 } moep_predict_args;
 
 int moep_predict_bf16(const moep_predict_args* a, void* stream);
+
+/* Scratch (floats) that lets moep_predict_bf16 split the hidden dimension
+ * over CTA pairs when N is too small to fill the GPU with 256-token tiles
+ * (partial logits per hidden group, summed in fixed order by a finish kernel
+ * that runs the same selection / margin / counter epilogue). 0: no split for
+ * this shape. Passing less than this in split_scratch_floats disables the split. */
+int64_t moep_predict_split_floats(int64_t n_tokens, int32_t hidden, int32_t n_experts);
 
 /* ------------------------------------------------------------------ K2 --
  * fp64 predictor on CUDA cores, mirroring the reference's float64 op order
@@ -122,7 +131,8 @@ int moep_predict_fp64(const moep_fp64_args* a, void* stream);
  * moep_decode_fp64 when *row_count <= 256 and by a register-blocked fp64 GEMM
  * otherwise (decided on the device), then a per-token finish kernel; rows
  * beyond the capacity go through moep_predict_fp64 with their evaluation
- * partials in partials2 ([moep_num_sms(), n_counters]).
+ * partials in partials2 ([moep_num_sms(), n_counters]; written only when
+ * capacity < N).
  * scratch: max(capacity * ceil(hidden/128), min(capacity, 256) * ceil(hidden/16)) * E doubles. */
 int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t capacity, int32_t* partials2,
                     void* stream);

@@ -32,7 +32,7 @@ class PredictArgs(C.Structure):
         ("tau_abs", f32), ("tau_rel", f32), ("w2_norm", f32),
         ("ids", vp), ("logits", vp), ("flags", vp), ("flag_list", vp), ("flag_count", vp),
         ("truth", vp), ("k", i32), ("n_m", i32), ("m_list", i32 * MAX_BOUNDS), ("partials", vp),
-        ("a_out", vp),
+        ("a_out", vp), ("split_scratch", vp), ("split_scratch_floats", i64),
     ]
 
 
@@ -73,6 +73,7 @@ _SIGS = {
     "moep_predict_fp64": [C.POINTER(Fp64Args), vp],
     "moep_fixup_fp64": [C.POINTER(Fp64Args), vp, i64, vp, vp],
     "moep_decode_fp64": [C.POINTER(Fp64Args), vp, vp],
+    "moep_predict_split_floats": [i64, i32, i32],
     "moep_eval_logits": [vp, i32, i64, i32, vp, i32, i32, vp, vp, vp],
     "moep_topk_logits": [vp, i32, i64, i32, i32, vp, vp],
     "moep_rank_order": [vp, i32, i64, i32, vp, vp],
@@ -92,7 +93,7 @@ _SIGS = {
     "moep_num_sms": [],
     "moep_version": [],
 }
-_RESTYPES = {"moep_version": C.c_char_p}
+_RESTYPES = {"moep_version": C.c_char_p, "moep_predict_split_floats": i64}
 EXPORTED = tuple(_SIGS)
 
 _lib = None

@@ -29,6 +29,11 @@ struct Params {
   int* partials;
   int n_counters;
   float* a_out;
+  // hidden split (pair kernel, small N): `split` chunk groups per 256-token tile;
+  // partial z [split][zpad][EP] and partial ||h||^2 [split][zpad] in zpart
+  int split;
+  float* zpart;
+  int64_t zpad;
 };
 
 // mbarrier wait that traps instead of hanging forever (a lost arrival becomes a

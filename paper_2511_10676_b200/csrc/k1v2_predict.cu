@@ -89,6 +89,9 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
   const int num_tiles = static_cast<int>((p.n_tokens + 2 * BM - 1) / (2 * BM));
   const int nchunks = p.hidden / HC;
   const int nk = (p.d + BK - 1) / BK;
+  // work item = (tile, chunk group): `split` groups of cpg chunks per tile
+  const int G = p.split, cpg = nchunks / G;
+  const int n_items = num_tiles * G;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -119,9 +122,10 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       if (elect_one()) {
         const uint64_t keep = policy_evict_last();
         uint32_t stage = 0, phase = 0;
-        for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+        for (int item = pair; item < n_items; item += n_pairs) {
+          const int tile = item / G, c0 = (item % G) * cpg;
           const int xrow = tile * 2 * BM + rank * BM;
-          for (int c = 0; c < nchunks; ++c) {
+          for (int c = c0; c < c0 + cpg; ++c) {
             const int wrow = c * HC + rank * HB;
             for (int kb = 0; kb < nk; ++kb) {
               wait(&empty[stage], phase ^ 1);
@@ -138,8 +142,9 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       if (elect_one()) {
         const uint64_t keep = policy_evict_last();
         uint32_t n = 0;
-        for (int tile = pair; tile < num_tiles; tile += n_pairs) {
-          for (int c = 0; c < nchunks; ++c, ++n) {
+        for (int item = pair; item < n_items; item += n_pairs) {
+          const int c0 = (item % G) * cpg;
+          for (int c = c0; c < c0 + cpg; ++c, ++n) {
             if (n > 0) wait(w2_empty, (n - 1) & 1);
             if (leader) mbar_arrive_expect_tx(w2_full, 2 * 4 * C::W2_ATOM);
 #pragma unroll
@@ -191,13 +196,13 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
             } else {
               umma_commit_mc(a2_emptyB, 0x3);
               umma_commit_mc(w2_empty, 0x3);
-              if (p_cc == nchunks - 1) umma_commit_mc(z_full, 0x3);
+              if (p_cc == cpg - 1) umma_commit_mc(z_full, 0x3);
             }
             ++p_half;
           }
         };
-        for (int tile = pair; tile < num_tiles; tile += n_pairs, ++ti) {
-          for (int c = 0; c < nchunks; ++c, ++gc) {
+        for (int item = pair; item < n_items; item += n_pairs, ++ti) {
+          for (int c = 0; c < cpg; ++c, ++gc) {  // c: chunk within the item
             wait(acc_empty, (gc & 1) ^ 1);
             tc_fence_after();
             for (int kb = 0; kb < nk; ++kb) {
@@ -235,10 +240,11 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
     RowCounters rc;
     rc.zero();
     uint32_t gc = 0, ti = 0;
-    for (int tile = pair; tile < num_tiles; tile += n_pairs, ++ti) {
+    for (int item = pair; item < n_items; item += n_pairs, ++ti) {
+      const int tile = item / G, grp = item % G, c0 = grp * cpg;
       const int64_t row_g = static_cast<int64_t>(tile) * 2 * BM + rank * BM + row_in_tile;
       float sumsq = 0.f;
-      for (int c = 0; c < nchunks; ++c, ++gc) {
+      for (int c = c0; c < c0 + cpg; ++c, ++gc) {
         wait(acc_full, gc & 1);
         tc_fence_after();
         float v[128];
@@ -327,14 +333,22 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(z_empty, 0);
-        // The A2 buffer is idle here: WG1 cannot write the next tile's A2 before
-        // GEMM2 half 0 of its chunk 0, which needs this warpgroup's half first.
-        uint32_t zswz;
-        float* zrow = k1c::zstage_row<EP>(smem + C::OFF_A2, row_in_tile, lane, zswz);
-        k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc, zrow, zswz);
+        if (G > 1) {
+          // hidden split: this group's partial z and ||h||^2 (split_finish sums the groups)
+          float* zp = p.zpart + (static_cast<int64_t>(grp) * p.zpad + row_g) * EP;
+#pragma unroll
+          for (int j = 0; j < EP; j += 4) *reinterpret_cast<float4*>(zp + j) = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
+          p.zpart[static_cast<int64_t>(G) * p.zpad * EP + static_cast<int64_t>(grp) * p.zpad + row_g] = sumsq;
+        } else {
+          // The A2 buffer is idle here: WG1 cannot write the next tile's A2 before
+          // GEMM2 half 0 of its chunk 0, which needs this warpgroup's half first.
+          uint32_t zswz;
+          float* zrow = k1c::zstage_row<EP>(smem + C::OFF_A2, row_in_tile, lane, zswz);
+          k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc, zrow, zswz);
+        }
       }
     }
-    if (wg == 0 && p.partials)
+    if (wg == 0 && p.partials && G == 1)
       k1c::write_partials<EP>(p, rc, q, lane, threadIdx.x - EPI_WARP0 * 32,
                               reinterpret_cast<int*>(smem + C::OFF_RED), hist0, 2);
   }
@@ -344,8 +358,77 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
   if (warp == 3) tmem_dealloc_cg2<512>(tmem);
 }
 
+// Hidden-split finish: z = fixed-order sum of the groups' partial logits, then
+// the same per-token selection / margin / counter epilogue as the fused path.
+// 128 threads = 4 warps, one token per thread; grid = num_SMs (one counter
+// partial row per CTA, the layout moep_counters_reduce expects).
+template <int EP>
+__global__ void __launch_bounds__(128) split_finish_kernel(const Params p) {
+  extern __shared__ __align__(16) uint8_t fsm[];
+  int* hist0 = reinterpret_cast<int*>(fsm);                 // [4][2][EP]
+  int* red0 = hist0 + 4 * 2 * EP;                           // [4][16]
+  uint8_t* zstage = reinterpret_cast<uint8_t*>(red0 + 64);  // 128 staging rows
+  const int tid = threadIdx.x, q = tid >> 5, lane = tid & 31;
+  int* hist = hist0 + q * 2 * EP;
+  for (int e = lane; e < 2 * EP; e += 32) hist[e] = 0;
+  __syncwarp();
+  RowCounters rc;
+  rc.zero();
+  const int G = p.split;
+  const float* sq = p.zpart + static_cast<int64_t>(G) * p.zpad * EP;
+  uint32_t zswz;
+  float* zrow = k1c::zstage_row<EP>(zstage, tid, lane, zswz);
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * 128; base < p.n_tokens;
+       base += static_cast<int64_t>(gridDim.x) * 128) {
+    const int64_t row = base + tid;
+    const bool valid = row < p.n_tokens;
+    float z[EP];
+#pragma unroll
+    for (int j = 0; j < EP; ++j) z[j] = 0.f;
+    float sumsq = 0.f;
+    if (valid) {
+      for (int g = 0; g < G; ++g) {
+        const float4* zp = reinterpret_cast<const float4*>(p.zpart + (static_cast<int64_t>(g) * p.zpad + row) * EP);
+#pragma unroll
+        for (int j = 0; j < EP / 4; ++j) {
+          const float4 v = __ldcg(zp + j);
+          z[4 * j] += v.x; z[4 * j + 1] += v.y; z[4 * j + 2] += v.z; z[4 * j + 3] += v.w;
+        }
+        sumsq += __ldcg(sq + static_cast<int64_t>(g) * p.zpad + row);
+      }
+    }
+    k1c::row_epilogue<EP>(p, z, sumsq, row, valid, lane, hist, rc, zrow, zswz);
+  }
+  if (p.partials) k1c::write_partials<EP>(p, rc, q, lane, tid, red0, hist0, 1);
+}
+
+// Chunk groups per tile: the fewest pair-rounds of chunks, ties to fewer groups.
+static int choose_split(int64_t n_tokens, int hidden, int n_pairs) {
+  const int nchunks = hidden / HC;
+  const int64_t tiles = (n_tokens + 2 * BM - 1) / (2 * BM);
+  int best = 1;
+  int64_t best_cost = ((tiles + n_pairs - 1) / n_pairs) * nchunks;
+  for (int g = 2; g <= nchunks && g <= 16; g *= 2) {
+    if (nchunks % g) continue;
+    const int64_t cost = ((tiles * g + n_pairs - 1) / n_pairs) * (nchunks / g);
+    if (cost < best_cost) { best = g; best_cost = cost; }
+  }
+  return best;
+}
+
 }  // namespace k1v2
 }  // namespace moep
+
+extern "C" int64_t moep_predict_split_floats(int64_t n_tokens, int32_t hidden, int32_t n_experts) {
+  using namespace moep::k1v2;
+  if (n_tokens <= 0 || hidden <= 0 || hidden % HC != 0 || n_experts <= 0 || n_experts > 128) return 0;
+  const int g = choose_split(n_tokens, hidden, moep_num_sms() / 2);
+  if (g == 1) return 0;
+  int EP = 16;
+  while (EP < n_experts) EP *= 2;
+  const int64_t zpad = ((n_tokens + 2 * BM - 1) / (2 * BM)) * 2 * BM;
+  return static_cast<int64_t>(g) * zpad * (EP + 1);
+}
 
 namespace {
 template <int EP, int ARCH>
@@ -377,8 +460,25 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
   p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;
   p.n_counters = moep_n_counters(a->n_m, a->n_experts);
   const int grid = moep_num_sms() & ~1;  // whole CTA pairs
+  p.split = 1; p.zpart = nullptr; p.zpad = 0;
+  const int64_t need = moep_predict_split_floats(a->n_tokens, a->hidden, a->n_experts);
+  if (need > 0 && a->split_scratch && a->split_scratch_floats >= need) {
+    p.split = choose_split(a->n_tokens, a->hidden, grid / 2);
+    p.zpart = a->split_scratch;
+    p.zpad = ((a->n_tokens + 2 * BM - 1) / (2 * BM)) * 2 * BM;
+  }
   kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);
-  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+  if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
+  if (p.split > 1) {
+    auto fin = split_finish_kernel<EP>;
+    const int fsmem = 4 * 2 * EP * 4 + 64 * 4 + 128 * (EP + 1) * 4;
+    if (fsmem > 48 * 1024 &&
+        cudaFuncSetAttribute(fin, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem) != cudaSuccess)
+      return MOEP_ELAUNCH;
+    fin<<<moep_num_sms(), 128, fsmem, st>>>(p);
+    if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
+  }
+  return MOEP_OK;
 }
 }  // namespace
 

@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(NT, 2)
 fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   extern __shared__ double sm[];
   const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
-  if (a.rows && count <= DEC_ROWS_MAX) return;  // dec_gemm's share
   const int64_t nrows = count < cap ? count : cap;
+  if (a.rows && nrows <= DEC_ROWS_MAX) return;  // dec_gemm's share
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * TM;
   if (r0 >= nrows) return;
   const int d = a.d, H = a.hidden, E = a.n_experts;
@@ -285,8 +285,8 @@ fix_finish(moep_fp64_args a, int64_t cap, int ntile_big, const double* __restric
   if (threadIdx.x < 2 + 2 * MOEP_MAX_BOUNDS) scal[threadIdx.x] = 0;
   __syncthreads();
   const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
-  if (!a.rows || count <= DEC_ROWS_MAX) return;  // dec_finish's share (it writes the partials)
   const int64_t nrows = count < cap ? count : cap;
+  if (!a.rows || nrows <= DEC_ROWS_MAX) return;  // dec_finish's share (it writes the partials)
   const int ntile_h = ntile_big;
   double* z = zsm + warp * E;
   int* rk = rkall + warp * E;
@@ -384,8 +384,9 @@ dec_finish(moep_fp64_args a, int64_t cap, int ntile, const double* __restrict__ 
   if (tid < 2 + 2 * MOEP_MAX_BOUNDS) scal[tid] = 0;
   __syncthreads();
   const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
-  const bool mine = !a.rows || count <= DEC_ROWS_MAX;
-  const int64_t nrows = !mine ? 0 : (count < cap ? count : cap);
+  const int64_t nall = count < cap ? count : cap;
+  const bool mine = !a.rows || nall <= DEC_ROWS_MAX;
+  const int64_t nrows = mine ? nall : 0;
   if (!mine && !a.partials) return;
   const int per = (ntile + G - 1) / G;
   for (int64_t it = blockIdx.x; it < nrows; it += gridDim.x) {
@@ -508,8 +509,8 @@ dec_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   const int d = a.d, H = a.hidden, E = a.n_experts;
   // rows mode (fix-up): list indices [0, min(count, cap)), only when count is small
   const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
-  if (a.rows && count > DEC_ROWS_MAX) return;
   const int64_t n = count < cap ? count : cap;
+  if (a.rows && n > DEC_ROWS_MAX) return;
   const int64_t t0 = static_cast<int64_t>(blockIdx.y) * TT;
   if (t0 >= n) return;
   __shared__ int64_t rowid[TT];
@@ -659,8 +660,8 @@ dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smb + rawb);        // [nseg]
   uint16_t* w2smem = (E % 8 == 0) ? reinterpret_cast<uint16_t*>(bars + 4) : nullptr;  // [DH][E]
   const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
-  if (a.rows && count > DEC_ROWS_MAX) return;
   const int64_t n = count < cap ? count : cap;
+  if (a.rows && n > DEC_ROWS_MAX) return;
   const int64_t t0 = static_cast<int64_t>(blockIdx.y) * TT;
   if (t0 >= n) return;
   __shared__ int64_t rowid[TT];
@@ -803,6 +804,8 @@ namespace k2b {
 // dec_gemm over list indices [0, cap): 8-token tiles for cap <= 8, else 32
 static int launch_dec(const moep_fp64_args* a, int64_t cap, double* scratch, cudaStream_t st) {
   const int ntile = (a->hidden + DH - 1) / DH;
+  // rows mode: the kernel only runs when min(count, cap) <= DEC_ROWS_MAX
+  const int64_t grid_rows = (a->rows && cap > DEC_ROWS_MAX) ? DEC_ROWS_MAX : cap;
   const bool xb = a->x_dtype == MOEP_BF16, wb = a->w_dtype == MOEP_BF16;
   // bulk-copy kernel: bf16 x and W1, d a multiple of DKC, 16-byte aligned rows
   const bool bulk_ok = xb && wb && (a->d % DKC) == 0 && (reinterpret_cast<uintptr_t>(a->x) & 15) == 0 &&
@@ -810,24 +813,24 @@ static int launch_dec(const moep_fp64_args* a, int64_t cap, double* scratch, cud
   auto gob = [&](auto kern, int tt, size_t smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
       return MOEP_ELAUNCH;
-    dim3 grid(static_cast<unsigned>(ntile), static_cast<unsigned>((cap + tt - 1) / tt));
+    dim3 grid(static_cast<unsigned>(ntile), static_cast<unsigned>((grid_rows + tt - 1) / tt));
     kern<<<grid, 256, smem, st>>>(*a, cap, scratch);
     return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
   };
   constexpr size_t kSmemMax = 227 * 1024;
-  if (bulk_ok && cap > 8 && dec_bulk_smem<16>(a->d, a->n_experts) <= kSmemMax)
+  if (bulk_ok && grid_rows > 8 && dec_bulk_smem<16>(a->d, a->n_experts) <= kSmemMax)
     return gob(dec_gemm_bulk<16>, 16, dec_bulk_smem<16>(a->d, a->n_experts));
-  if (bulk_ok && cap <= 8 && dec_bulk_smem<8>(a->d, a->n_experts) <= kSmemMax)
+  if (bulk_ok && grid_rows <= 8 && dec_bulk_smem<8>(a->d, a->n_experts) <= kSmemMax)
     return gob(dec_gemm_bulk<8>, 8, dec_bulk_smem<8>(a->d, a->n_experts));
   auto go = [&](auto kern, int tt) {
     const size_t smem = sizeof(double) * 2 * DKC * (tt + DH);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
       return MOEP_ELAUNCH;
-    dim3 grid(static_cast<unsigned>(ntile), static_cast<unsigned>((cap + tt - 1) / tt));
+    dim3 grid(static_cast<unsigned>(ntile), static_cast<unsigned>((grid_rows + tt - 1) / tt));
     kern<<<grid, 256, smem, st>>>(*a, cap, scratch);
     return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
   };
-  if (cap <= 8) {
+  if (grid_rows <= 8) {
     if (xb && wb) return go(dec_gemm<MOEP_BF16, MOEP_BF16, 8>, 8);
     if (xb) return go(dec_gemm<MOEP_BF16, MOEP_F64, 8>, 8);
     if (wb) return go(dec_gemm<MOEP_F64, MOEP_BF16, 8>, 8);
@@ -899,18 +902,24 @@ extern "C" int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t
     kern<<<grid, NT, smem, st>>>(*a, cap, scratch);
     return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
   };
-  int rc;
-  if (xb && wb) rc = go(fix_gemm<MOEP_BF16, MOEP_BF16>);
-  else if (xb) rc = go(fix_gemm<MOEP_BF16, MOEP_F64>);
-  else if (wb) rc = go(fix_gemm<MOEP_F64, MOEP_BF16>);
-  else rc = go(fix_gemm<MOEP_F64, MOEP_F64>);
+  // min(count, capacity) <= DEC_ROWS_MAX (decided on the device): the
+  // split-hidden kernel; larger: the GEMM. With capacity <= DEC_ROWS_MAX the
+  // GEMM and its finish kernel can never run and are not launched.
+  const bool big = cap > DEC_ROWS_MAX;
+  int rc = MOEP_OK;
+  if (big) {
+    if (xb && wb) rc = go(fix_gemm<MOEP_BF16, MOEP_BF16>);
+    else if (xb) rc = go(fix_gemm<MOEP_BF16, MOEP_F64>);
+    else if (wb) rc = go(fix_gemm<MOEP_F64, MOEP_BF16>);
+    else rc = go(fix_gemm<MOEP_F64, MOEP_F64>);
+    if (rc != MOEP_OK) return rc;
+  }
+  rc = launch_dec(a, cap, scratch, st);
   if (rc != MOEP_OK) return rc;
-  // small flagged counts (decided on the device): the split-hidden kernel
-  rc = launch_dec(a, cap < DEC_ROWS_MAX ? cap : DEC_ROWS_MAX, scratch, st);
-  if (rc != MOEP_OK) return rc;
-  rc = launch_finish(a, cap, scratch, st, true);  // the device count picks the finish kernel
+  rc = launch_finish(a, cap, scratch, st, big);
   if (rc != MOEP_OK) return rc;
   // rows beyond the scratch capacity: the per-group kernel, starting at row `cap`
+  if (cap >= a->n_tokens) return MOEP_OK;  // no overflow possible; partials2 untouched
   moep_fp64_args b = *a;
   b.row_begin = cap;
   b.partials = partials2;

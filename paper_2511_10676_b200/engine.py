@@ -240,6 +240,10 @@ class DevicePredictor:
         for i, m in enumerate(m_values):
             a.m_list[i] = m
         a.partials = ptr(partials)
+        # small N: scratch that lets the kernel split the hidden dimension over CTA pairs
+        need = int(lib().moep_predict_split_floats(n, self.hidden, self.E)) if self.split_hidden else 0
+        scratch = torch.empty(need, dtype=torch.float32, device=self.device) if need else None
+        a.split_scratch, a.split_scratch_floats = ptr(scratch), need
         check(lib().moep_predict_bf16(a, _stream(self.device)), "moep_predict_bf16")
         return flags, flag_list, flag_count
 
@@ -249,13 +253,18 @@ class DevicePredictor:
                 and all(p <= K1_MAX_SEL or p >= self.E for p in positions))
 
     decode_max_tokens = DECODE_MAX_TOKENS  # 0 forces the tensor-core path for every batch
-    fixup_capacity = None  # rows handled by the GEMM fix-up per call (None: max(2048, N/128))
+    split_hidden = True  # let K1 split the hidden dimension when N is small (False: one pair per tile)
+    fixup_capacity = None  # rows handled by the fast fix-up per call (None: max(min(N, 64), N/128))
+
+    def _fixup_cap(self, n):
+        # flagged rows are ~0.3 % of N: the capacity bounds the split-hidden /
+        # GEMM fix-up grid; rows beyond it take the (slower) overflow kernel
+        cap = self.fixup_capacity or max(min(n, 64), n // 128)
+        return min(cap, n)
 
     def _fixup(self, a, n, partials2=None):
-        """Exact fp64 recompute of K1's flagged rows (fast GEMM path + overflow)."""
-        cap = self.fixup_capacity or max(2048, n // 128)
-        if cap > n:
-            cap = n
+        """Exact fp64 recompute of K1's flagged rows (fast path + overflow)."""
+        cap = self._fixup_cap(n)
         size = max(cap * ((self.hidden + 127) // 128), min(cap, 256) * ((self.hidden + 15) // 16)) * self.E
         scratch = torch.empty(size, dtype=torch.float64, device=self.device)
         check(lib().moep_fixup_fp64(a, ptr(scratch), cap, ptr(partials2), _stream(self.device)),
@@ -357,7 +366,8 @@ class DevicePredictor:
                                 truth=truth, k=k, m_values=m_values,
                                 partials=partials[self.n_sms: 2 * self.n_sms])
             self._fixup(a, n, partials2=partials[2 * self.n_sms:])
-            check(lib().moep_counters_reduce(ptr(partials), 3 * self.n_sms, ncnt, ptr(counters),
+            nrow = 3 if self._fixup_cap(n) < n else 2  # overflow partials only when they can exist
+            check(lib().moep_counters_reduce(ptr(partials), nrow * self.n_sms, ncnt, ptr(counters),
                                              _stream(self.device)), "moep_counters_reduce")
             return counters, fcount, ids
         # general path: exact fp64 logits for every token, then K7 from logits

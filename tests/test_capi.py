@@ -16,7 +16,7 @@ HEADER = os.path.join(ROOT, "include", "moep_b200.h")
 def declared_symbols():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    names = set(re.findall(r"\b(?:int|const char\*)\s+(moep_\w+)\s*\(", text))
+    names = set(re.findall(r"\b(?:int|int64_t|const char\*)\s+(moep_\w+)\s*\(", text))
     return sorted(names)
 
 

@@ -164,6 +164,34 @@ def test_margin_covers_error(pb, O):
     assert 2 * ratio.max() < TAU_REL, ratio.max()
 
 
+@pytest.mark.parametrize("n,e", [(256, 64), (4096, 64), (8192, 128), (300, 16)])
+def test_margin_covers_error_hidden_split(pb, O, n, e):
+    """Same guard for the hidden-split K1 (small N: partial logits per hidden
+    group summed in fp32 by the finish kernel), and the split path equals the
+    unsplit one on ids."""
+    from paper_2511_10676_b200 import _lib
+    from paper_2511_10676_b200.engine import TAU_REL
+    d = h = 2048
+    assert _lib.lib().moep_predict_split_floats(n, h, e) > 0
+    rng = np.random.default_rng(n + e)
+    m = bf16_model(pb, O, "arch2", d, h, e, seed=6)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref, cache = O.forward_eval(oracle_params(m), x)
+    dev = m.to_device()
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    lg = torch.empty((n, e), dtype=torch.float32, device="cuda")
+    dev._k1(xt, logits=lg)
+    err = np.abs(lg.double().cpu().numpy() - zref).max(axis=1)
+    scale = np.linalg.norm(cache["h"], axis=1) * np.linalg.norm(m.w2, axis=1).max()
+    assert 2 * (err / scale).max() < TAU_REL, (err / scale).max()
+    dev.decode_max_tokens = 0
+    ids_split = dev.topk(xt, 6).cpu().numpy()
+    dev.split_hidden = False
+    ids_flat = dev.topk(xt, 6).cpu().numpy()
+    assert np.array_equal(ids_split, O.top_k_batch(zref, 6))
+    assert np.array_equal(ids_split, ids_flat)
+
+
 def test_ties_go_to_fp64_and_lower_index(pb, O):
     """Duplicate W2 rows give exact logit ties; the lower expert index must win."""
     rng = np.random.default_rng(3)
@@ -237,7 +265,7 @@ def test_fixup_overflow_path(pb, O, tau_rel, lo, hi):
     truth = O.top_k_batch(zref + 0.05 * rng.standard_normal(zref.shape), 6)
     ms = [6, 10, 64]
     oc = O.eval_counters(zref, truth, 64, ms)
-    for cap in (None, 8):
+    for cap in (None, 8, 4096):
         dev = m.to_device(tau_rel=tau_rel)
         dev.fixup_capacity = cap
         xt = torch.from_numpy(x).to("cuda", torch.bfloat16)

@@ -13,12 +13,13 @@ for name, E, k in (("qwen3", 128, 8), ("dsv2l", 64, 6)):
     m = pb.init_model("arch2", 2048, 2048, E, seed=1)
     m.w1, m.w2 = O.round_bf16(m.w1), O.round_bf16(m.w2)
     dev = m.to_device()
-    for n in (1, 2, 4, 8, 16, 32, 64, 128, 256):
+    for n in (1, 2, 4, 8, 16, 32, 64, 128, 256, 1024, 4096, 16384, 65536):
         x = torch.randn((n, 2048), device="cuda").to(torch.bfloat16)
         row = {"shape": name, "batch": n}
         for path, lim in (("decode_fp64", 1 << 30), ("tensor_k1", 0)):
             if path == "decode_fp64" and n > 256:
                 continue
+            flop = 2 * n * (2048 * 2048 + 2048 * E)
             dev.decode_max_tokens = lim
             for _ in range(10):
                 dev.topk(x, k, validate=False)
@@ -49,5 +50,6 @@ for name, E, k in (("qwen3", 128, 8), ("dsv2l", 64, 6)):
             b.record()
             torch.cuda.synchronize()
             row[path + "_graph_us"] = a.elapsed_time(b) / 200 * 1e3
+            row[path + "_tflops"] = flop / (row[path + "_graph_us"] * 1e-6) / 1e12
         res.append(row)
         print(json.dumps(row), flush=True)
