@@ -322,9 +322,10 @@ def cpu_baseline(model, x, truth, n_sample=32768):
 
 
 def prefetch_arm(dp, x, dev, batches=(1, 8, 32, 128, 256)):
-    """Predicted-expert prefetch (BASELINE configs[4]): DSV2L expert blobs
-    (17,301,504 B) from pinned host memory into a device cache, for the union of
-    the predicted top-6 sets of B tokens, vs the measured host-link H2D peak.
+    """Predicted-expert prefetch (BASELINE configs[4]): DSV2L (17,301,504 B) and
+    Qwen3 (9,437,184 B) expert blobs from pinned host memory into a device cache,
+    for the union of the predicted top-k sets of B tokens, vs the measured
+    host-link H2D peak.
     Also the attention overlap at B=1: stall = max(0, load_end - attention_end)."""
     import torch
     import torch.nn.functional as F
@@ -347,16 +348,34 @@ def prefetch_arm(dp, x, dev, batches=(1, 8, 32, 128, 256)):
         b.synchronize()
         return a.elapsed_time(b)
 
-    for B in batches:
-        ids = dp.topk(x[:B], K_ACT)
-        for path in ("copy_engine", "sm_gather"):
-            fn = (lambda: p.load_copy_engine(ids)) if path == "copy_engine" else (lambda: p.load_sm_gather(ids, 148))
-            timed(fn)  # warm
-            ms = min(timed(fn) for _ in range(3))
-            n = int(p.need_count.item())
-            gbs = n * pf.DSV2L_EXPERT_BYTES / (ms / 1e3) / 1e9
-            out["sweep"].append({"batch_tokens": B, "path": path, "experts_loaded": n,
-                                 "bytes": n * pf.DSV2L_EXPERT_BYTES, "ms": ms, "gbs": gbs, "frac": gbs / peak})
+    def sweep(shape, pred, k, prefetcher, eb):
+        nonlocal p
+        p_saved, p = p, prefetcher
+        for B in batches:
+            ids = pred.topk(x[:B], k)
+            for path in ("copy_engine", "sm_gather"):
+                fn = (lambda: p.load_copy_engine(ids)) if path == "copy_engine" else (lambda: p.load_sm_gather(ids, 148))
+                timed(fn)  # warm
+                ms = min(timed(fn) for _ in range(3))
+                n = int(p.need_count.item())
+                gbs = n * eb / (ms / 1e3) / 1e9
+                out["sweep"].append({"shape": shape, "batch_tokens": B, "path": path, "experts_loaded": n,
+                                     "expert_bytes": eb, "bytes": n * eb, "ms": ms, "gbs": gbs, "frac": gbs / peak})
+        p = p_saved
+
+    sweep("DeepSeek-V2-Lite (E=64, top-6)", dp, K_ACT, p, pf.DSV2L_EXPERT_BYTES)
+    # Qwen3-30B-A3B experts (E=128, top-8, 9,437,184 B each) from a Qwen3-shaped predictor
+    import paper_2511_10676_b200 as pb
+    qm = pb.init_model("arch2", D, H, 128, seed=1)
+    qm.w1, qm.w2 = _round_bf16_np(qm.w1), _round_bf16_np(qm.w2)
+    qdp = pb.DevicePredictor(qm, dev)
+    qstore = pf.ExpertStore(128, pf.QWEN3_EXPERT_BYTES)
+    qcache = pf.ExpertCache(128, pf.QWEN3_EXPERT_BYTES, 128, device=dev)
+    cache_saved = cache
+    cache = qcache
+    sweep("Qwen3-30B-A3B (E=128, top-8)", qdp, 8, pf.Prefetcher(qstore, qcache), pf.QWEN3_EXPERT_BYTES)
+    cache = cache_saved
+    del qstore, qcache
     # overlap with an attention stand-in (decode, B=1: 16 q heads, 16 kv heads, head_dim 128,
     # 4096 cached tokens; DeepSeek-V2-Lite MLA is approximated by plain SDPA)
     q = torch.randn(1, 16, 1, 128, device=dev, dtype=torch.bfloat16)
@@ -370,11 +389,13 @@ def prefetch_arm(dp, x, dev, batches=(1, 8, 32, 128, 256)):
     t0 = torch.cuda.Event(enable_timing=True)
     t_attn, t_load = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(main)
-    p.copy.wait_event(t0)
-    p.load_sm_gather(ids, 148)
-    t_load.record(p.copy)
     F.scaled_dot_product_attention(q, kv, kv)  # this layer's attention: the prefetch window
     t_attn.record(main)
+    # copy engines, so the attention keeps every SM: the host reads the tiny
+    # plan (it waits for the plan only) and queues one copy per missing expert
+    p.copy.wait_event(t0)
+    p.load_copy_engine(ids)
+    t_load.record(p.copy)
     torch.cuda.synchronize()
     la, ll = t0.elapsed_time(t_attn), t0.elapsed_time(t_load)
     out["overlap_b1"] = {"attention_ms": la, "load_ms": ll, "stall_ms": max(0.0, ll - la),

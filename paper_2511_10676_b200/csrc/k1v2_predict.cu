@@ -402,10 +402,14 @@ __global__ void __launch_bounds__(128) split_finish_kernel(const Params p) {
   if (p.partials) k1c::write_partials<EP>(p, rc, q, lane, tid, red0, hist0, 1);
 }
 
-// Chunk groups per tile: the fewest pair-rounds of chunks, ties to fewer groups.
+// Chunk groups per tile: only when the tiles leave CTA pairs idle (fewer tiles
+// than pairs); then the fewest pair-rounds of chunks, ties to fewer groups.
+// Large N never splits (the partial-logit traffic and the x re-streaming would
+// cost more than the last-wave imbalance they remove).
 static int choose_split(int64_t n_tokens, int hidden, int n_pairs) {
   const int nchunks = hidden / HC;
   const int64_t tiles = (n_tokens + 2 * BM - 1) / (2 * BM);
+  if (tiles >= n_pairs) return 1;
   int best = 1;
   int64_t best_cost = ((tiles + n_pairs - 1) / n_pairs) * nchunks;
   for (int g = 2; g <= nchunks && g <= 16; g *= 2) {
