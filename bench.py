@@ -125,6 +125,17 @@ def make_layers(dev, n_layers, tokens, seed_base):
     return layers
 
 
+def _k1_traffic(tokens):
+    """DRAM bytes per K1 launch from the committed ncu capture (None if absent)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_k1_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t["traffic_bytes"] * tokens / t["tokens_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def _round_bf16_np(a):
     a = np.asarray(a, dtype=np.float64)
     m, e = np.frexp(a)
@@ -256,10 +267,14 @@ def main():
                          "frac": achieved_tflops / sustained, "peak_kind": f"{src} sustained bf16",
                          "frac_of_burst": achieved_tflops / burst, "kernel": "moep k1 predict_kernel",
                          "flop_per_token": FLOP_PER_TOKEN, "tokens_per_launch": args.tokens,
-                         "k1_ms_per_launch": k1_ms, "pipeline_ms_per_layer": pipe_ms, "traffic": None},
-            # per layer: K1 pair kernel, fix-up GEMM, fix-up finish, overflow K2 (no-op unless
-            # the scratch overflows), counter reduce
-            "gpu_launches": args.steps * args.layers * 5,
+                         "k1_ms_per_launch": k1_ms, "pipeline_ms_per_layer": pipe_ms,
+                         "traffic": _k1_traffic(args.tokens),
+                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch, "
+                                           "ncu --set full (profiles/r01_k1_traffic.json), scaled to tokens"},
+            # per layer: K1 pair kernel; fix-up: GEMM, split-hidden kernel + its finish (exit
+            # at once unless <= 256 rows are flagged), GEMM finish, overflow K2 (exits unless
+            # the capacity overflows); counter reduce
+            "gpu_launches": args.steps * args.layers * 7,
             "clocks": clk.summary(),
             "flagged_fraction": flagged / (args.layers * args.tokens * world),
             "id_match": id_match,
