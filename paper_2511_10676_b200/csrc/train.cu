@@ -212,12 +212,19 @@ __global__ void finalize_kernel(const double* __restrict__ partials, int nblk, i
 
 // ------------------------------------------------------------------ K5
 // One thread per hidden column j, a CTA covers 128 columns x a slice of rows.
-// Writes dA (fp32) and per-slice partials of dW2 [E, h], db1 [h], db2 [E].
-template <int EMAX, typename T>
+// Writes dA and per-slice partials of dW2 [E, h], db1 [h], db2 [E]. Rows go
+// in groups of RU with the group's `a` loads issued together (memory-level
+// parallelism: the kernel streams a and dA at HBM rate). SPLIT: dA is written
+// as bf16 hi (rows 0..n-1) and lo = bf16(dA - hi) (rows n..2n-1) of a [2n, h]
+// buffer row-wise: row n = [hi(dA[n, :]) | lo(dA[n, :])] of a [n, 2h] bf16
+// buffer, the operand of the bf16 dW1 GEMM (fp32 mode).
+template <int EMAX, typename T, bool SPLIT>
 __global__ void __launch_bounds__(128)
 act_backward_kernel(const T* __restrict__ a, const T* __restrict__ dz, const T* __restrict__ w2,
                     int64_t n, int H, int E, int rows_per_slice, T* __restrict__ da,
-                    T* __restrict__ dw2_part, T* __restrict__ db1_part, T* __restrict__ db2_part) {
+                    __nv_bfloat16* __restrict__ da_hilo, T* __restrict__ dw2_part, T* __restrict__ db1_part,
+                    T* __restrict__ db2_part) {
+  constexpr int RU = 8;
   __shared__ T sdz[32][EMAX];
   const int j = blockIdx.x * 128 + threadIdx.x;
   const int slice = blockIdx.y;
@@ -239,24 +246,39 @@ act_backward_kernel(const T* __restrict__ a, const T* __restrict__ dz, const T* 
     __syncthreads();
     if (j < H) {
       const int lim = (r1 - rb < 32) ? static_cast<int>(r1 - rb) : 32;
-      for (int rr = 0; rr < lim; ++rr) {
-        const int64_t row = rb + rr;
-        const T av = a[row * H + j];
-        // branch-stable sigmoid (predictor.py:39-45), silu / silu' (:48-54)
-        T sg;
-        if (av >= T(0)) sg = T(1) / (T(1) + exp(-av));
-        else { const T ea = exp(av); sg = ea / (T(1) + ea); }
-        const T hv = av * sg;
-        const T dsilu = sg * (T(1) + av * (T(1) - sg));
-        T dh = T(0);
+      for (int rg = 0; rg < lim; rg += RU) {
+        T av[RU];
 #pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-          dh = fma(sdz[rr][e], w2c[e], dh);
-          acc[e] = fma(sdz[rr][e], hv, acc[e]);
+        for (int u = 0; u < RU; ++u) av[u] = (rg + u < lim) ? a[(rb + rg + u) * H + j] : T(0);
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          if (rg + u < lim) {
+            const int rr = rg + u;
+            const int64_t row = rb + rr;
+            const T x = av[u];
+            // branch-stable sigmoid (predictor.py:39-45), silu / silu' (:48-54)
+            T sg;
+            if (x >= T(0)) sg = T(1) / (T(1) + exp(-x));
+            else { const T ea = exp(x); sg = ea / (T(1) + ea); }
+            const T hv = x * sg;
+            const T dsilu = sg * (T(1) + x * (T(1) - sg));
+            T dh = T(0);
+#pragma unroll
+            for (int e = 0; e < EMAX; ++e) {
+              dh = fma(sdz[rr][e], w2c[e], dh);
+              acc[e] = fma(sdz[rr][e], hv, acc[e]);
+            }
+            const T dav = dh * dsilu;
+            if constexpr (SPLIT) {
+              const __nv_bfloat16 hi = __float2bfloat16_rn(static_cast<float>(dav));
+              da_hilo[row * 2 * H + j] = hi;
+              da_hilo[row * 2 * H + H + j] = __float2bfloat16_rn(static_cast<float>(dav) - __bfloat162float(hi));
+            } else {
+              da[row * H + j] = dav;
+            }
+            db1 += dav;
+          }
         }
-        const T dav = dh * dsilu;
-        da[row * H + j] = dav;
-        db1 += dav;
       }
     }
   }
@@ -273,14 +295,156 @@ act_backward_kernel(const T* __restrict__ a, const T* __restrict__ dz, const T* 
   }
 }
 
+// packed fp32x2 FMA (sm_100 FFMA2): two lanes of work per instruction
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+        "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+// fp32 / bf16-split variant: two adjacent hidden columns per thread (float2
+// loads of a, each dz value from smem feeds both columns) and a branch-free
+// stable sigmoid (e = exp(-|x|); sigmoid = x >= 0 ? 1/(1+e) : e/(1+e)) with
+// the fast exp / reciprocal -- the fp32 mode's tolerance, not the fp64 path.
+template <int EMAX>
+__global__ void __launch_bounds__(128)
+act_backward_f32x2_kernel(const float* __restrict__ a, const float* __restrict__ dz, const float* __restrict__ w2,
+                          int64_t n, int H, int E, int rows_per_slice, __nv_bfloat16* __restrict__ da_hilo,
+                          float* __restrict__ dw2_part, float* __restrict__ db1_part, float* __restrict__ db2_part) {
+  constexpr int RU = 4;
+  __shared__ __align__(16) float2 sdz2[32][EMAX];       // dz values duplicated {g, g}: FFMA2 operands
+  const int j = (blockIdx.x * 128 + threadIdx.x) * 2;   // columns j, j+1 (H even)
+  const int slice = blockIdx.y;
+  const int64_t r0 = static_cast<int64_t>(slice) * rows_per_slice;
+  const int64_t r1 = (r0 + rows_per_slice < n) ? r0 + rows_per_slice : n;
+  const bool ok = j < H;
+  float2 w01[EMAX], acc[EMAX];  // (column j, column j+1) pairs
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) {
+    w01[e] = (ok && e < E) ? *reinterpret_cast<const float2*>(w2 + static_cast<int64_t>(e) * H + j)
+                           : make_float2(0.f, 0.f);
+    acc[e] = make_float2(0.f, 0.f);
+  }
+  float2 db1 = make_float2(0.f, 0.f);
+  // one row: sigmoid / silu / silu' (branch-free stable form), dH = dz . W2 in 4
+  // independent FFMA2 chains (fixed order), dW2 += dz (x) h, hi/lo bf16 stores
+  auto row_step = [&](float2 x2, int rr, const float* /*unused*/, __nv_bfloat16* hp, __nv_bfloat16* lp) {
+    const float xs[2] = {x2.x, x2.y};
+    float hv[2], ds[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const float x = xs[c];
+      const float ex = __expf(-fabsf(x));
+      const float r = __frcp_rn(1.f + ex);
+      const float sg = x >= 0.f ? r : ex * r;
+      hv[c] = x * sg;
+      ds[c] = sg * (1.f + x * (1.f - sg));
+    }
+    const float2 h2 = make_float2(hv[0], hv[1]);
+    float2 dhp[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+    for (int e2 = 0; e2 < EMAX; e2 += 2) {
+      const float4 gg = *reinterpret_cast<const float4*>(&sdz2[rr][e2]);
+      const float2 g0 = make_float2(gg.x, gg.y), g1 = make_float2(gg.z, gg.w);
+      dhp[e2 & 3] = ffma2(g0, w01[e2], dhp[e2 & 3]);
+      dhp[(e2 + 1) & 3] = ffma2(g1, w01[e2 + 1], dhp[(e2 + 1) & 3]);
+      acc[e2] = ffma2(g0, h2, acc[e2]);
+      acc[e2 + 1] = ffma2(g1, h2, acc[e2 + 1]);
+    }
+    const float d0 = ((dhp[0].x + dhp[1].x) + (dhp[2].x + dhp[3].x)) * ds[0];
+    const float d1 = ((dhp[0].y + dhp[1].y) + (dhp[2].y + dhp[3].y)) * ds[1];
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(d0, d1);
+    const float2 hf = __bfloat1622float2(hi);
+    *reinterpret_cast<__nv_bfloat162*>(hp) = hi;
+    *reinterpret_cast<__nv_bfloat162*>(lp) = __floats2bfloat162_rn(d0 - hf.x, d1 - hf.y);
+    db1.x += d0;
+    db1.y += d1;
+  };
+  for (int64_t rb = r0; rb < r1; rb += 32) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * EMAX; i += 128) {
+      const int rr = i / EMAX, e = i % EMAX;
+      const float g = (rb + rr < r1 && e < E) ? dz[(rb + rr) * E + e] : 0.f;
+      sdz2[rr][e] = make_float2(g, g);
+    }
+    __syncthreads();
+    if (!ok) continue;
+    const int lim = (r1 - rb < 32) ? static_cast<int>(r1 - rb) : 32;
+    const float* ap = a + rb * H + j;
+    __nv_bfloat16* hp = da_hilo + rb * 2 * H + j;      // row layout [hi(0..H) | lo(0..H)]
+    __nv_bfloat16* lp = hp + H;
+    const int rs = 2 * H;
+    if (lim == 32) {
+      // software pipeline: the next RU rows' loads are in flight while this group computes
+      float2 cur[RU], nxt[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) cur[u] = __ldcs(reinterpret_cast<const float2*>(ap + u * H));
+#pragma unroll 1
+      for (int rg = 0; rg < 32; rg += RU) {
+        if (rg + RU < 32) {
+#pragma unroll
+          for (int u = 0; u < RU; ++u) nxt[u] = __ldcs(reinterpret_cast<const float2*>(ap + (rg + RU + u) * H));
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) row_step(cur[u], rg + u, nullptr, hp + (rg + u) * rs, lp + (rg + u) * rs);
+#pragma unroll
+        for (int u = 0; u < RU; ++u) cur[u] = nxt[u];
+      }
+    } else {
+      for (int rr = 0; rr < lim; ++rr)
+        row_step(*reinterpret_cast<const float2*>(ap + rr * H), rr, nullptr, hp + rr * rs, lp + rr * rs);
+    }
+  }
+  if (ok) {
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e)
+      if (e < E) *reinterpret_cast<float2*>(dw2_part + (static_cast<int64_t>(slice) * E + e) * H + j) = acc[e];
+    *reinterpret_cast<float2*>(db1_part + static_cast<int64_t>(slice) * H + j) = db1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < E) {
+    float sacc = 0.f;
+    for (int64_t row = r0; row < r1; ++row) sacc += dz[row * E + threadIdx.x];
+    db2_part[static_cast<int64_t>(slice) * E + threadIdx.x] = sacc;
+  }
+}
+
+// dW2 / db1 / db2 slice sums in one launch: element i of the concatenation
+// [E*H | H | E] reads its own segment's partials (fixed slice order).
 template <typename T>
-__global__ void sum_slices_kernel(const T* __restrict__ part, int nslice, int64_t len, T* __restrict__ out) {
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+__global__ void sum_slices3_kernel(const T* __restrict__ p0, const T* __restrict__ p1, const T* __restrict__ p2,
+                                   int nslice, int64_t l0, int64_t l1, int64_t l2, T* __restrict__ o0,
+                                   T* __restrict__ o1, T* __restrict__ o2) {
+  const int64_t tot = l0 + l1 + l2;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < tot;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const T* part;
+    T* out;
+    int64_t i, len;
+    if (g < l0) { part = p0; out = o0; i = g; len = l0; }
+    else if (g < l0 + l1) { part = p1; out = o1; i = g - l0; len = l1; }
+    else { part = p2; out = o2; i = g - l0 - l1; len = l2; }
     T s = T(0);
-    for (int k = 0; k < nslice; ++k) s += part[k * len + i];
+    int k = 0;
+    for (; k + 8 <= nslice; k += 8) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + (k + u) * len + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; k < nslice; ++k) s += part[k * len + i];
     out[i] = s;
   }
+}
+
+template <typename T>
+static void sum_parts3(const T* dw2_part, const T* db1_part, const T* db2_part, int n_slices, int E, int H, T* dw2,
+                       T* db1, T* db2, cudaStream_t st) {
+  sum_slices3_kernel<T><<<moep_num_sms() * 2, 256, 0, st>>>(dw2_part, db1_part, db2_part, n_slices,
+                                                            static_cast<int64_t>(E) * H, H, E, dw2, db1, db2);
 }
 
 // ------------------------------------------------------------------ K6
@@ -391,22 +555,22 @@ int moep_loss_finalize(const double* partials, int32_t n_blocks, int64_t n, int3
 
 }  // extern "C"
 
-template <typename T>
+template <typename T, bool SPLIT>
 static int act_backward_t(const T* a, const T* dz, const T* w2, int64_t n, int32_t H, int32_t E, int32_t n_slices,
-                          T* da, T* dw2, T* db1, T* db2, T* scratch, cudaStream_t st) {
+                          T* da, __nv_bfloat16* da_hilo, T* dw2, T* db1, T* db2, T* scratch, cudaStream_t st) {
   const int rows_per_slice = static_cast<int>((n + n_slices - 1) / n_slices);
   T* dw2_part = scratch;
   T* db1_part = dw2_part + static_cast<int64_t>(n_slices) * E * H;
   T* db2_part = db1_part + static_cast<int64_t>(n_slices) * H;
   dim3 grid((H + 127) / 128, n_slices);
-  if (E <= 16) act_backward_kernel<16, T><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, da, dw2_part, db1_part, db2_part);
-  else if (E <= 32) act_backward_kernel<32, T><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, da, dw2_part, db1_part, db2_part);
-  else if (E <= 64) act_backward_kernel<64, T><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, da, dw2_part, db1_part, db2_part);
-  else act_backward_kernel<128, T><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, da, dw2_part, db1_part, db2_part);
-  const int g2 = moep_num_sms() * 2;
-  sum_slices_kernel<T><<<g2, 256, 0, st>>>(dw2_part, n_slices, static_cast<int64_t>(E) * H, dw2);
-  sum_slices_kernel<T><<<g2, 256, 0, st>>>(db1_part, n_slices, H, db1);
-  sum_slices_kernel<T><<<1, 256, 0, st>>>(db2_part, n_slices, E, db2);
+#define MOEP_K5(EM) act_backward_kernel<EM, T, SPLIT><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, da, \
+                                                                          da_hilo, dw2_part, db1_part, db2_part)
+  if (E <= 16) MOEP_K5(16);
+  else if (E <= 32) MOEP_K5(32);
+  else if (E <= 64) MOEP_K5(64);
+  else MOEP_K5(128);
+#undef MOEP_K5
+  sum_parts3<T>(dw2_part, db1_part, db2_part, n_slices, E, H, dw2, db1, db2, st);
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }
 
@@ -419,16 +583,40 @@ int moep_act_backward(const void* a, const void* dz, const void* w2, int32_t dty
   if (E > 128) return MOEP_EUNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (dtype == MOEP_F64)
-    return act_backward_t<double>(static_cast<const double*>(a), static_cast<const double*>(dz),
-                                  static_cast<const double*>(w2), n, H, E, n_slices, static_cast<double*>(da),
-                                  static_cast<double*>(dw2), static_cast<double*>(db1), static_cast<double*>(db2),
-                                  static_cast<double*>(scratch), st);
+    return act_backward_t<double, false>(static_cast<const double*>(a), static_cast<const double*>(dz),
+                                         static_cast<const double*>(w2), n, H, E, n_slices, static_cast<double*>(da),
+                                         nullptr, static_cast<double*>(dw2), static_cast<double*>(db1),
+                                         static_cast<double*>(db2), static_cast<double*>(scratch), st);
   if (dtype == MOEP_F32)
-    return act_backward_t<float>(static_cast<const float*>(a), static_cast<const float*>(dz),
-                                 static_cast<const float*>(w2), n, H, E, n_slices, static_cast<float*>(da),
-                                 static_cast<float*>(dw2), static_cast<float*>(db1), static_cast<float*>(db2),
-                                 static_cast<float*>(scratch), st);
+    return act_backward_t<float, false>(static_cast<const float*>(a), static_cast<const float*>(dz),
+                                        static_cast<const float*>(w2), n, H, E, n_slices, static_cast<float*>(da),
+                                        nullptr, static_cast<float*>(dw2), static_cast<float*>(db1),
+                                        static_cast<float*>(db2), static_cast<float*>(scratch), st);
   return MOEP_EARG;
+}
+
+int moep_act_backward_bf16split(const float* a, const float* dz, const float* w2, int64_t n, int32_t H, int32_t E,
+                                int32_t n_slices, void* da_hilo, float* dw2, float* db1, float* db2, float* scratch,
+                                void* stream) {
+  if (n <= 0 || H <= 0 || E <= 0 || n_slices <= 0) return MOEP_ESHAPE;
+  if (E > 128) return MOEP_EUNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(da_hilo);
+  if (H % 2 != 0 || E > 32)
+    return act_backward_t<float, true>(a, dz, w2, n, H, E, n_slices, nullptr, out, dw2, db1, db2, scratch, st);
+  const int rows_per_slice = static_cast<int>((n + n_slices - 1) / n_slices);
+  float* dw2_part = scratch;
+  float* db1_part = dw2_part + static_cast<int64_t>(n_slices) * E * H;
+  float* db2_part = db1_part + static_cast<int64_t>(n_slices) * H;
+  dim3 grid((H / 2 + 127) / 128, n_slices);
+  if (E <= 16)
+    act_backward_f32x2_kernel<16><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, out, dw2_part, db1_part,
+                                                        db2_part);
+  else
+    act_backward_f32x2_kernel<32><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, out, dw2_part, db1_part,
+                                                        db2_part);
+  sum_parts3<float>(dw2_part, db1_part, db2_part, n_slices, E, H, dw2, db1, db2, st);
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }
 
 int moep_optim_step(const moep_optim_args* a, void* stream) {

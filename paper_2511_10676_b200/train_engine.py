@@ -166,25 +166,43 @@ class DeviceTrainer:
                                          int(cache.get("training", True)), _stream(self.dev)), "moep_bn_backward")
             torch.sum(dz, dim=0, out=self.view(self.grad, 3))
         else:
-            n_slices = max(1, min(64, n // 256))
-            da = torch.empty((n, H), dtype=self.dt, device=self.dev)
+            # row slices: enough CTAs to fill the GPU (the x2 fp32 kernel has half the columns per CTA)
+            n_slices = max(1, min(64 if self.precision == "fp64" else 128, n // 128))
             scratch = torch.empty(n_slices * (E * H + H + E), dtype=self.dt, device=self.dev)
-            check(lib().moep_act_backward(ptr(cache["a"]), ptr(dz), ptr(self.view(self.flat, 1)), dtype_code(dz), n,
-                                          H, E, n_slices, ptr(da), ptr(self.view(self.grad, 1)),
-                                          ptr(self.view(self.grad, 2)), ptr(self.view(self.grad, 3)), ptr(scratch),
-                                          _stream(self.dev)), "moep_act_backward")
+            if self.precision == "fp64":
+                da = torch.empty((n, H), dtype=self.dt, device=self.dev)
+                check(lib().moep_act_backward(ptr(cache["a"]), ptr(dz), ptr(self.view(self.flat, 1)),
+                                              dtype_code(dz), n, H, E, n_slices, ptr(da), ptr(self.view(self.grad, 1)),
+                                              ptr(self.view(self.grad, 2)), ptr(self.view(self.grad, 3)),
+                                              ptr(scratch), _stream(self.dev)), "moep_act_backward")
+            else:
+                # dA leaves K5 as bf16 hi / lo halves: the dW1 GEMM operands directly
+                da = torch.empty((n, 2 * H), dtype=torch.bfloat16, device=self.dev)
+                check(lib().moep_act_backward_bf16split(ptr(cache["a"]), ptr(dz), ptr(self.view(self.flat, 1)), n,
+                                                        H, E, n_slices, ptr(da), ptr(self.view(self.grad, 1)),
+                                                        ptr(self.view(self.grad, 2)), ptr(self.view(self.grad, 3)),
+                                                        ptr(scratch), _stream(self.dev)),
+                      "moep_act_backward_bf16split")
         gw1 = self.view(self.grad, 0)
         if self.precision == "fp64":
             xs = x_used if x_used.dtype == torch.float64 else x_used.to(torch.float64)
             torch.mm(da.t(), xs, out=gw1)  # plain fp64 GEMM (cuBLAS DGEMM)
-        else:
-            # dW1 = dA^T X on bf16 tensor cores: dA split hi + lo, fp32 accumulate/output
+        elif self.arch == "arch1":
             hi = da.to(torch.bfloat16)
             lo = (da - hi.float()).to(torch.bfloat16)
-            a2 = torch.cat([hi, lo], dim=0)                    # [2n, H]
-            x2 = torch.cat([x_used, x_used], dim=0)            # [2n, d] bf16 (exact inputs)
-            gw1.copy_(torch.mm(a2.t(), x2, out_dtype=torch.float32))
+            self._dw1_hilo(hi, lo, x_used, gw1)
+        else:
+            # one bf16 GEMM over the [hi | lo] rows: C = [hi^T X ; lo^T X], fp32
+            c = torch.mm(da.t(), x_used, out_dtype=torch.float32)
+            torch.add(c[:H], c[H:], out=gw1)
         return da
+
+    @staticmethod
+    def _dw1_hilo(hi, lo, x, gw1):
+        """dW1 = hi^T X + lo^T X on bf16 tensor cores, fp32 accumulate (cuBLAS,
+        the second GEMM accumulating into the first's output)."""
+        acc = torch.mm(hi.t(), x, out_dtype=torch.float32)
+        gw1.copy_(torch.addmm(acc, lo.t(), x, out_dtype=torch.float32))
 
     # -------------------------------------------------------------- step
     def optimizer_step(self):
