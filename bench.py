@@ -167,6 +167,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-prefetch", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -245,6 +246,9 @@ def main():
             cpu = cpu_baseline(layers[0][0], layers[0][2], layers[0][3], n_sample=32768)
     if not args.no_e2e:
         e2e = e2e_arm(layers, args, world, dev)
+    train = None
+    if not args.no_train:
+        train = train_arm(args, rank, world, dev)
     prefetch = None
     if rank == 0 and not args.no_prefetch:
         prefetch = prefetch_arm(layers[0][1], layers[0][2], dev)
@@ -283,6 +287,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "prefetch": prefetch,
+            "train": train,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -475,6 +480,61 @@ def e2e_arm(layers, args, world, dev):
     return {"value": world * tokens * args.layers * steps / (ms / 1e3), "unit": "tokens/s",
             "h2d_bytes_per_step": bytes_in, "d2h_bytes_per_step": bytes_out, "steps": steps,
             "api": "DevicePredictor.evaluate on device buffers filled from pinned host memory"}
+
+
+def train_arm(args, rank, world, dev, n_local=16384, steps=10):
+    """BASELINE configs[3]: Phi-mini-shaped predictor training (d=4096, h=2048,
+    E=16, k=2, arch2 + ranking-aware loss, Adam), data parallel: every rank
+    trains on its own n_local tokens per step (weak scaling), loss partial sums
+    and the flat fp32 gradient all-reduced over NCCL each step. One step =
+    K1 forward (pre-activations) + K3/K4 loss + K5 + dW1 GEMM + all-reduce + K6."""
+    import torch
+    import torch.distributed as dist
+    import paper_2511_10676_b200 as pb
+    d, h, e, k = 4096, 2048, 16, 2
+    m = pb.init_model("arch2", d, h, e, seed=7)          # same weights on every rank
+    m.w1, m.w2 = _round_bf16_np(m.w1), _round_bf16_np(m.w2)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5000 + rank)
+    x = torch.randn((n_local, d), device=dev, generator=g).to(torch.bfloat16)
+    gate = torch.randn((e, d), device=dev, generator=g) / np.sqrt(d)
+    scores = torch.softmax(x.float() @ gate.T, dim=1)
+    lab = pb.BatchLabels.from_scores(scores.double(), k)
+    sc = lab.true_scores.to(torch.float32).contiguous()
+    mk = lab.topk_mask.to(torch.uint8).contiguous()
+    rk = lab.rank_of.contiguous()
+    from paper_2511_10676_b200.distributed import dp_hooks
+    hooks = dp_hooks() if world > 1 else (None, None)
+    tr = pb.DeviceTrainer(m, pb.LossSpec(family="ranking"), "adam", 1e-3, precision="fp32",
+                          grad_allreduce=hooks[0], loss_allreduce=hooks[1], device=dev)
+    n_global = n_local * world
+    for _ in range(3):
+        tr.step(x, sc, mk, rk, n_global=n_global)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(steps):
+        out = tr.step(x, sc, mk, rk, n_global=n_global)
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    burst, sustained, _, src = peaks()
+    flop_tok = 4 * d * h + 6 * h * e
+    tps = n_global / (ms / 1e3)
+    return {"workload": "Phi-mini shape (d=4096, h=2048, E=16, k=2) arch2 + ranking-aware loss, Adam "
+                        "(BASELINE configs[3])",
+            "precision": "fp32 master, bf16 tensor-core GEMMs (hi/lo split operands)",
+            "tokens_per_step": n_global, "ms_per_step": ms, "tokens_per_s": tps,
+            "scaling": "weak", "grad_allreduce": "NCCL fp32 flat buffer" if world > 1 else "none (1 rank)",
+            "flop_per_token": flop_tok,
+            "roofline": {"bound": "tensor", "achieved": tps * flop_tok / 1e12 / world, "peak": sustained,
+                         "unit": "TFLOP/s per GPU", "frac": tps * flop_tok / 1e12 / world / sustained},
+            "final_loss": float(out[0].item())}
 
 
 # ------------------------------------------------------------- reference arm
