@@ -508,21 +508,28 @@ def train_arm(args, rank, world, dev, n_local=16384, steps=10):
     tr = pb.DeviceTrainer(m, pb.LossSpec(family="ranking"), "adam", 1e-3, precision="fp32",
                           grad_allreduce=hooks[0], loss_allreduce=hooks[1], device=dev)
     n_global = n_local * world
-    for _ in range(3):
-        tr.step(x, sc, mk, rk, n_global=n_global)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    a.record()
-    for _ in range(steps):
-        out = tr.step(x, sc, mk, rk, n_global=n_global)
-    b.record()
-    torch.cuda.synchronize()
-    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item()) / steps
+
+    def run(trainer):
+        for _ in range(3):
+            trainer.step(x, sc, mk, rk, n_global=n_global)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(steps):
+            res = trainer.step(x, sc, mk, rk, n_global=n_global)
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / steps, res
+
+    ms, out = run(tr)
+    tr16 = pb.DeviceTrainer(m, pb.LossSpec(family="ranking"), "adam", 1e-3, precision="bf16",
+                            grad_allreduce=hooks[0], loss_allreduce=hooks[1], device=dev)
+    ms16, _ = run(tr16)
     burst, sustained, _, src = peaks()
     flop_tok = 4 * d * h + 6 * h * e
     tps = n_global / (ms / 1e3)
@@ -534,7 +541,9 @@ def train_arm(args, rank, world, dev, n_local=16384, steps=10):
             "flop_per_token": flop_tok,
             "roofline": {"bound": "tensor", "achieved": tps * flop_tok / 1e12 / world, "peak": sustained,
                          "unit": "TFLOP/s per GPU", "frac": tps * flop_tok / 1e12 / world / sustained},
-            "final_loss": float(out[0].item())}
+            "final_loss": float(out[0].item()),
+            "bf16_grad_operand": {"ms_per_step": ms16, "tokens_per_s": n_global / (ms16 / 1e3),
+                                  "note": "precision='bf16': dW1 GEMM on bf16(dA) only (no lo half)"}}
 
 
 # ------------------------------------------------------------- reference arm

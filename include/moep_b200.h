@@ -219,13 +219,14 @@ int moep_act_backward(const void* a, const void* dz, const void* w2, int32_t dty
                       void* db1, void* db2, void* scratch, void* stream);
 
 /* K5, fp32 training mode: same as moep_act_backward (dtype fp32) but dA is
- * written as bf16 pairs: row i of da_hilo [n, 2*hidden] is
+ * written as bf16: with_lo != 0: row i of da_hilo [n, 2*hidden] is
  * [hi = bf16(dA[i, :]) | lo = bf16(dA[i, :] - hi)] -- one bf16 tensor-core GEMM
  * C = da_hilo^T X ([2h, d], fp32) then gives dW1 = C[:h] + C[h:] (no fp32 dA
- * round trip through HBM, no duplicated X). */
+ * round trip through HBM, no duplicated X); with_lo == 0: da_hilo [n, hidden]
+ * holds hi only (bf16 gradient operand, the "bf16" training precision). */
 int moep_act_backward_bf16split(const float* a, const float* dz, const float* w2, int64_t n, int32_t hidden,
-                                int32_t n_experts, int32_t n_slices, void* da_hilo, float* dw2, float* db1,
-                                float* db2, float* scratch, void* stream);
+                                int32_t n_experts, int32_t n_slices, int32_t with_lo, void* da_hilo, float* dw2,
+                                float* db1, float* db2, float* scratch, void* stream);
 
 /* K6: optimizer step on a flat master buffer (trainer.py:103-122).
  * kind: 0 sgd, 1 momentum, 2 adam (bias-corrected with step t, 1-based).

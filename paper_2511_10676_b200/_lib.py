@@ -83,7 +83,7 @@ _SIGS = {
     "moep_loss": [C.POINTER(LossArgs), vp],
     "moep_loss_finalize": [vp, i32, i64, i32, i32, f64, i32, i32, vp, vp, vp, vp],
     "moep_act_backward": [vp, vp, vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
-    "moep_act_backward_bf16split": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
+    "moep_act_backward_bf16split": [vp, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp],
     "moep_optim_step": [C.POINTER(OptimArgs), vp],
     "moep_bn_forward": [vp, i64, i32, vp, vp, vp, vp, f64, f64, f64, C.c_uint64, C.c_uint64, vp, vp, vp, vp,
                         vp, vp, i32, vp],

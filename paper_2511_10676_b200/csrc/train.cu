@@ -309,7 +309,7 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 // loads of a, each dz value from smem feeds both columns) and a branch-free
 // stable sigmoid (e = exp(-|x|); sigmoid = x >= 0 ? 1/(1+e) : e/(1+e)) with
 // the fast exp / reciprocal -- the fp32 mode's tolerance, not the fp64 path.
-template <int EMAX>
+template <int EMAX, bool LO>
 __global__ void __launch_bounds__(128)
 act_backward_f32x2_kernel(const float* __restrict__ a, const float* __restrict__ dz, const float* __restrict__ w2,
                           int64_t n, int H, int E, int rows_per_slice, __nv_bfloat16* __restrict__ da_hilo,
@@ -359,7 +359,7 @@ act_backward_f32x2_kernel(const float* __restrict__ a, const float* __restrict__
     const __nv_bfloat162 hi = __floats2bfloat162_rn(d0, d1);
     const float2 hf = __bfloat1622float2(hi);
     *reinterpret_cast<__nv_bfloat162*>(hp) = hi;
-    *reinterpret_cast<__nv_bfloat162*>(lp) = __floats2bfloat162_rn(d0 - hf.x, d1 - hf.y);
+    if constexpr (LO) *reinterpret_cast<__nv_bfloat162*>(lp) = __floats2bfloat162_rn(d0 - hf.x, d1 - hf.y);
     db1.x += d0;
     db1.y += d1;
   };
@@ -374,9 +374,9 @@ act_backward_f32x2_kernel(const float* __restrict__ a, const float* __restrict__
     if (!ok) continue;
     const int lim = (r1 - rb < 32) ? static_cast<int>(r1 - rb) : 32;
     const float* ap = a + rb * H + j;
-    __nv_bfloat16* hp = da_hilo + rb * 2 * H + j;      // row layout [hi(0..H) | lo(0..H)]
+    const int rs = LO ? 2 * H : H;                     // row layout [hi(0..H) | lo(0..H)] or [hi]
+    __nv_bfloat16* hp = da_hilo + rb * rs + j;
     __nv_bfloat16* lp = hp + H;
-    const int rs = 2 * H;
     if (lim == 32) {
       // software pipeline: the next RU rows' loads are in flight while this group computes
       float2 cur[RU], nxt[RU];
@@ -596,25 +596,26 @@ int moep_act_backward(const void* a, const void* dz, const void* w2, int32_t dty
 }
 
 int moep_act_backward_bf16split(const float* a, const float* dz, const float* w2, int64_t n, int32_t H, int32_t E,
-                                int32_t n_slices, void* da_hilo, float* dw2, float* db1, float* db2, float* scratch,
-                                void* stream) {
+                                int32_t n_slices, int32_t with_lo, void* da_hilo, float* dw2, float* db1, float* db2,
+                                float* scratch, void* stream) {
   if (n <= 0 || H <= 0 || E <= 0 || n_slices <= 0) return MOEP_ESHAPE;
   if (E > 128) return MOEP_EUNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(da_hilo);
-  if (H % 2 != 0 || E > 32)
+  if (H % 2 != 0 || E > 32) {
+    if (!with_lo) return MOEP_EUNSUPPORTED;
     return act_backward_t<float, true>(a, dz, w2, n, H, E, n_slices, nullptr, out, dw2, db1, db2, scratch, st);
+  }
   const int rows_per_slice = static_cast<int>((n + n_slices - 1) / n_slices);
   float* dw2_part = scratch;
   float* db1_part = dw2_part + static_cast<int64_t>(n_slices) * E * H;
   float* db2_part = db1_part + static_cast<int64_t>(n_slices) * H;
   dim3 grid((H / 2 + 127) / 128, n_slices);
-  if (E <= 16)
-    act_backward_f32x2_kernel<16><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, out, dw2_part, db1_part,
-                                                        db2_part);
-  else
-    act_backward_f32x2_kernel<32><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, rows_per_slice, out, dw2_part, db1_part,
-                                                        db2_part);
+#define MOEP_K5X2(EM, LOV) act_backward_f32x2_kernel<EM, LOV><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, \
+                                   rows_per_slice, out, dw2_part, db1_part, db2_part)
+  if (E <= 16) { if (with_lo) MOEP_K5X2(16, true); else MOEP_K5X2(16, false); }
+  else { if (with_lo) MOEP_K5X2(32, true); else MOEP_K5X2(32, false); }
+#undef MOEP_K5X2
   sum_parts3<float>(dw2_part, db1_part, db2_part, n_slices, E, H, dw2, db1, db2, st);
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }

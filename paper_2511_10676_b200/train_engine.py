@@ -41,7 +41,10 @@ class DeviceTrainer:
     def __init__(self, model, loss: LossSpec, optimizer="adam", lr=1e-3, momentum=0.9, beta1=0.9,
                  beta2=0.999, eps=1e-8, precision="fp32", device="cuda", grad_allreduce=None,
                  loss_allreduce=None):
-        if precision not in ("fp32", "fp64"):
+        # fp64: exact parity mode (the reference's arithmetic); fp32: fp32 master
+        # weights, bf16 tensor-core GEMMs with hi/lo split operands; bf16: as fp32
+        # but the dW1 GEMM takes dA rounded to bf16 (no lo half: half the GEMM)
+        if precision not in ("fp32", "fp64", "bf16"):
             raise ConfigurationError(f"unknown precision {precision!r}")
         if model.arch == "arch1" and precision != "fp64":
             raise ConfigurationError("arch1 (batch-norm) training runs in the fp64 mode")
@@ -68,7 +71,7 @@ class DeviceTrainer:
         self.m = torch.zeros_like(self.flat)
         self.v = torch.zeros_like(self.flat) if self.kind == 2 else None
         self.n_shadow = H * d + E * H
-        self.shadow = self.flat[: self.n_shadow].to(torch.bfloat16) if precision == "fp32" else None
+        self.shadow = self.flat[: self.n_shadow].to(torch.bfloat16) if precision != "fp64" else None
         if self.arch == "arch1":
             f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(self.dev)
             self.run_mean, self.run_var = f64(model.bn_mean), f64(model.bn_var)
@@ -111,7 +114,7 @@ class DeviceTrainer:
         """Train-mode forward: logits [N, E], the cache the backward needs, and
         the activations actually used."""
         n = x.shape[0]
-        if self.precision == "fp32":
+        if self.precision != "fp64":
             xb = x if x.dtype == torch.bfloat16 else x.to(torch.bfloat16)
             z = torch.empty((n, self.E), dtype=torch.float32, device=self.dev)
             a_pre = torch.empty((n, self.H), dtype=torch.float32, device=self.dev)
@@ -176,10 +179,12 @@ class DeviceTrainer:
                                               ptr(self.view(self.grad, 2)), ptr(self.view(self.grad, 3)),
                                               ptr(scratch), _stream(self.dev)), "moep_act_backward")
             else:
-                # dA leaves K5 as bf16 hi / lo halves: the dW1 GEMM operands directly
-                da = torch.empty((n, 2 * H), dtype=torch.bfloat16, device=self.dev)
+                # dA leaves K5 as bf16 hi (| lo) halves: the dW1 GEMM operands directly
+                lo = self.precision == "fp32"
+                da = torch.empty((n, (2 if lo else 1) * H), dtype=torch.bfloat16, device=self.dev)
                 check(lib().moep_act_backward_bf16split(ptr(cache["a"]), ptr(dz), ptr(self.view(self.flat, 1)), n,
-                                                        H, E, n_slices, ptr(da), ptr(self.view(self.grad, 1)),
+                                                        H, E, n_slices, int(lo), ptr(da),
+                                                        ptr(self.view(self.grad, 1)),
                                                         ptr(self.view(self.grad, 2)), ptr(self.view(self.grad, 3)),
                                                         ptr(scratch), _stream(self.dev)),
                       "moep_act_backward_bf16split")
@@ -191,6 +196,8 @@ class DeviceTrainer:
             hi = da.to(torch.bfloat16)
             lo = (da - hi.float()).to(torch.bfloat16)
             self._dw1_hilo(hi, lo, x_used, gw1)
+        elif self.precision == "bf16":
+            gw1.copy_(torch.mm(da.t(), x_used, out_dtype=torch.float32))
         else:
             # one bf16 GEMM over the [hi | lo] rows: C = [hi^T X ; lo^T X], fp32
             c = torch.mm(da.t(), x_used, out_dtype=torch.float32)
