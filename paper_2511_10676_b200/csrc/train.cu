@@ -309,13 +309,16 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 // loads of a, each dz value from smem feeds both columns) and a branch-free
 // stable sigmoid (e = exp(-|x|); sigmoid = x >= 0 ? 1/(1+e) : e/(1+e)) with
 // the fast exp / reciprocal -- the fp32 mode's tolerance, not the fp64 path.
+constexpr int BR = 16;  // rows per staged block
+
 template <int EMAX, bool LO>
 __global__ void __launch_bounds__(128)
 act_backward_f32x2_kernel(const float* __restrict__ a, const float* __restrict__ dz, const float* __restrict__ w2,
                           int64_t n, int H, int E, int rows_per_slice, __nv_bfloat16* __restrict__ da_hilo,
                           float* __restrict__ dw2_part, float* __restrict__ db1_part, float* __restrict__ db2_part) {
-  constexpr int RU = 4;
-  __shared__ __align__(16) float2 sdz2[32][EMAX];       // dz values duplicated {g, g}: FFMA2 operands
+  __shared__ __align__(16) float2 sdz2[2][BR][EMAX];    // dz values duplicated {g, g}: FFMA2 operands
+  extern __shared__ __align__(16) float abuf_raw[];
+  auto abuf = reinterpret_cast<float(*)[BR][256]>(abuf_raw);  // [2][BR][256] staged rows of a
   const int j = (blockIdx.x * 128 + threadIdx.x) * 2;   // columns j, j+1 (H even)
   const int slice = blockIdx.y;
   const int64_t r0 = static_cast<int64_t>(slice) * rows_per_slice;
@@ -331,14 +334,16 @@ act_backward_f32x2_kernel(const float* __restrict__ a, const float* __restrict__
   float2 db1 = make_float2(0.f, 0.f);
   // one row: sigmoid / silu / silu' (branch-free stable form), dH = dz . W2 in 4
   // independent FFMA2 chains (fixed order), dW2 += dz (x) h, hi/lo bf16 stores
-  auto row_step = [&](float2 x2, int rr, const float* /*unused*/, __nv_bfloat16* hp, __nv_bfloat16* lp) {
+  auto row_step = [&](float2 x2, int sb, int rr, __nv_bfloat16* hp, __nv_bfloat16* lp) {
     const float xs[2] = {x2.x, x2.y};
     float hv[2], ds[2];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const float x = xs[c];
-      const float ex = __expf(-fabsf(x));
-      const float r = __frcp_rn(1.f + ex);
+      // e = 2^(-|x| log2 e), r = 1 / (1 + e): one MUFU op each, no slow paths
+      float ex, r;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"(-fabsf(x) * 1.4426950408889634f));
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + ex));
       const float sg = x >= 0.f ? r : ex * r;
       hv[c] = x * sg;
       ds[c] = sg * (1.f + x * (1.f - sg));
@@ -347,7 +352,7 @@ act_backward_f32x2_kernel(const float* __restrict__ a, const float* __restrict__
     float2 dhp[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
     for (int e2 = 0; e2 < EMAX; e2 += 2) {
-      const float4 gg = *reinterpret_cast<const float4*>(&sdz2[rr][e2]);
+      const float4 gg = *reinterpret_cast<const float4*>(&sdz2[sb][rr][e2]);
       const float2 g0 = make_float2(gg.x, gg.y), g1 = make_float2(gg.z, gg.w);
       dhp[e2 & 3] = ffma2(g0, w01[e2], dhp[e2 & 3]);
       dhp[(e2 + 1) & 3] = ffma2(g1, w01[e2 + 1], dhp[(e2 + 1) & 3]);
@@ -363,40 +368,69 @@ act_backward_f32x2_kernel(const float* __restrict__ a, const float* __restrict__
     db1.x += d0;
     db1.y += d1;
   };
-  for (int64_t rb = r0; rb < r1; rb += 32) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < 32 * EMAX; i += 128) {
-      const int rr = i / EMAX, e = i % EMAX;
-      const float g = (rb + rr < r1 && e < E) ? dz[(rb + rr) * E + e] : 0.f;
-      sdz2[rr][e] = make_float2(g, g);
-    }
-    __syncthreads();
-    if (!ok) continue;
-    const int lim = (r1 - rb < 32) ? static_cast<int>(r1 - rb) : 32;
-    const float* ap = a + rb * H + j;
-    const int rs = LO ? 2 * H : H;                     // row layout [hi(0..H) | lo(0..H)] or [hi]
-    __nv_bfloat16* hp = da_hilo + rb * rs + j;
-    __nv_bfloat16* lp = hp + H;
-    if (lim == 32) {
-      // software pipeline: the next RU rows' loads are in flight while this group computes
-      float2 cur[RU], nxt[RU];
-#pragma unroll
-      for (int u = 0; u < RU; ++u) cur[u] = __ldcs(reinterpret_cast<const float2*>(ap + u * H));
-#pragma unroll 1
-      for (int rg = 0; rg < 32; rg += RU) {
-        if (rg + RU < 32) {
-#pragma unroll
-          for (int u = 0; u < RU; ++u) nxt[u] = __ldcs(reinterpret_cast<const float2*>(ap + (rg + RU + u) * H));
-        }
-#pragma unroll
-        for (int u = 0; u < RU; ++u) row_step(cur[u], rg + u, nullptr, hp + (rg + u) * rs, lp + (rg + u) * rs);
-#pragma unroll
-        for (int u = 0; u < RU; ++u) cur[u] = nxt[u];
+  // BR-row blocks of this CTA's 256 columns of `a` stream through a double
+  // buffer with cp.async (16-byte chunks, whole block in flight), the next
+  // block's dz rows ride in registers; HBM latency overlaps the compute.
+  const int cb = blockIdx.x * 256;
+  const int ncols = (H - cb) < 256 ? (H - cb) : 256;   // even
+  const int nchunk = ncols / 4;                         // 16-byte chunks per row (H % 4 == 0)
+  auto issue = [&](int buf, int64_t rb) {
+    const int lim = (r1 - rb < BR) ? static_cast<int>(r1 - rb) : BR;
+    for (int c = threadIdx.x; c < BR * 64; c += 128) {
+      const int row = c >> 6, ch = c & 63;
+      if (row < lim && ch < nchunk) {
+        const float* src = a + (rb + row) * H + cb + ch * 4;
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&abuf[buf][row][ch * 4]));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
       }
-    } else {
-      for (int rr = 0; rr < lim; ++rr)
-        row_step(*reinterpret_cast<const float2*>(ap + rr * H), rr, nullptr, hp + rr * rs, lp + rr * rs);
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  constexpr int DZPT = BR * EMAX / 128;                 // dz values per thread per block
+  float dzr[DZPT];
+  auto load_dz = [&](int64_t rb) {
+#pragma unroll
+    for (int q = 0; q < DZPT; ++q) {
+      const int i = threadIdx.x + 128 * q, rr = i / EMAX, e = i % EMAX;
+      dzr[q] = (rb + rr < r1 && e < E) ? dz[(rb + rr) * E + e] : 0.f;
+    }
+  };
+  auto store_dz = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < DZPT; ++q) {
+      const int i = threadIdx.x + 128 * q, rr = i / EMAX, e = i % EMAX;
+      sdz2[buf][rr][e] = make_float2(dzr[q], dzr[q]);
+    }
+  };
+  if (r0 < r1) {
+    issue(0, r0);
+    load_dz(r0);
+    store_dz(0);
+  }
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += BR, buf ^= 1) {
+    const bool more = rb + BR < r1;
+    if (more) {
+      issue(buf ^ 1, rb + BR);
+      load_dz(rb + BR);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const int lim = (r1 - rb < BR) ? static_cast<int>(r1 - rb) : BR;
+    if (ok) {
+      const int rs = LO ? 2 * H : H;                   // row layout [hi(0..H) | lo(0..H)] or [hi]
+      __nv_bfloat16* hp = da_hilo + rb * rs + j;
+      __nv_bfloat16* lp = hp + H;
+#pragma unroll 2
+      for (int rr = 0; rr < lim; ++rr) {
+        const float2 x2 = *reinterpret_cast<const float2*>(&abuf[buf][rr][2 * threadIdx.x]);
+        row_step(x2, buf, rr, hp + rr * rs, lp + rr * rs);
+      }
+    }
+    if (more) store_dz(buf ^ 1);
+    __syncthreads();
   }
   if (ok) {
 #pragma unroll
@@ -602,7 +636,7 @@ int moep_act_backward_bf16split(const float* a, const float* dz, const float* w2
   if (E > 128) return MOEP_EUNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(da_hilo);
-  if (H % 2 != 0 || E > 32) {
+  if (H % 4 != 0 || E > 32) {
     if (!with_lo) return MOEP_EUNSUPPORTED;
     return act_backward_t<float, true>(a, dz, w2, n, H, E, n_slices, nullptr, out, dw2, db1, db2, scratch, st);
   }
@@ -611,8 +645,15 @@ int moep_act_backward_bf16split(const float* a, const float* dz, const float* w2
   float* db1_part = dw2_part + static_cast<int64_t>(n_slices) * E * H;
   float* db2_part = db1_part + static_cast<int64_t>(n_slices) * H;
   dim3 grid((H / 2 + 127) / 128, n_slices);
-#define MOEP_K5X2(EM, LOV) act_backward_f32x2_kernel<EM, LOV><<<grid, 128, 0, st>>>(a, dz, w2, n, H, E, \
-                                   rows_per_slice, out, dw2_part, db1_part, db2_part)
+  constexpr int kAbuf = 2 * BR * 256 * 4;  // staging for `a`
+#define MOEP_K5X2(EM, LOV)                                                                                     \
+  do {                                                                                                         \
+    if (cudaFuncSetAttribute(act_backward_f32x2_kernel<EM, LOV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             kAbuf) != cudaSuccess)                                                            \
+      return MOEP_ELAUNCH;                                                                                     \
+    act_backward_f32x2_kernel<EM, LOV><<<grid, 128, kAbuf, st>>>(a, dz, w2, n, H, E, rows_per_slice, out,      \
+                                                                  dw2_part, db1_part, db2_part);               \
+  } while (0)
   if (E <= 16) { if (with_lo) MOEP_K5X2(16, true); else MOEP_K5X2(16, false); }
   else { if (with_lo) MOEP_K5X2(32, true); else MOEP_K5X2(32, false); }
 #undef MOEP_K5X2
