@@ -359,47 +359,205 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
 }
 
 // Hidden-split finish: z = fixed-order sum of the groups' partial logits, then
-// the same per-token selection / margin / counter epilogue as the fused path.
-// 128 threads = 4 warps, one token per thread; grid = num_SMs (one counter
-// partial row per CTA, the layout moep_counters_reduce expects).
+// the per-token selection / margin / output / counter semantics of
+// k1c::row_epilogue (the fused path's epilogue), re-laid for one WARP per token
+// (lane l holds experts l, l+32, ...): the top list is built by warp argmax
+// reductions (value, then lower index on ties; -0.0 == +0.0), ascending ids by
+// ballot prefix sums, truth-expert lookups by shuffles. grid = num_SMs (one
+// counter partial row per CTA, the layout moep_counters_reduce expects).
 template <int EP>
-__global__ void __launch_bounds__(128) split_finish_kernel(const Params p) {
-  extern __shared__ __align__(16) uint8_t fsm[];
-  int* hist0 = reinterpret_cast<int*>(fsm);                 // [4][2][EP]
-  int* red0 = hist0 + 4 * 2 * EP;                           // [4][16]
-  uint8_t* zstage = reinterpret_cast<uint8_t*>(red0 + 64);  // 128 staging rows
-  const int tid = threadIdx.x, q = tid >> 5, lane = tid & 31;
-  int* hist = hist0 + q * 2 * EP;
-  for (int e = lane; e < 2 * EP; e += 32) hist[e] = 0;
-  __syncwarp();
+__global__ void __launch_bounds__(256) split_finish_kernel(const Params p) {
+  constexpr int PL = EP >= 32 ? EP / 32 : 1;   // experts per lane
+  __shared__ int hist_s[2 * EP];
+  __shared__ int cnt_s[2 + 2 * MOEP_MAX_BOUNDS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 2 * EP; i += 256) hist_s[i] = 0;
+  if (tid < 2 + 2 * MOEP_MAX_BOUNDS) cnt_s[tid] = 0;
+  __syncthreads();
+  const int G = p.split, E = p.E;
+  const float* sq = p.zpart + static_cast<int64_t>(G) * p.zpad * EP;
+  int P = p.m_sel;
+#pragma unroll
+  for (int b = 0; b < MOEP_MAX_BOUNDS; ++b)
+    if (b < p.n_bounds && p.bounds[b] > P) P = p.bounds[b];
+  P = min(P + 1, min(E, kMaxSel));
   RowCounters rc;
   rc.zero();
-  const int G = p.split;
-  const float* sq = p.zpart + static_cast<int64_t>(G) * p.zpad * EP;
-  uint32_t zswz;
-  float* zrow = k1c::zstage_row<EP>(zstage, tid, lane, zswz);
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * 128; base < p.n_tokens;
-       base += static_cast<int64_t>(gridDim.x) * 128) {
-    const int64_t row = base + tid;
-    const bool valid = row < p.n_tokens;
-    float z[EP];
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * 8;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp; row < p.n_tokens; row += nw) {
+    float zv[PL];
+    bool bad = false;
 #pragma unroll
-    for (int j = 0; j < EP; ++j) z[j] = 0.f;
+    for (int q = 0; q < PL; ++q) {
+      const int e = q * 32 + lane;
+      float acc = 0.f;
+      if (e < EP) {
+        // all groups' partials in flight together, then the fixed-order sum
+        float v[16];
+#pragma unroll
+        for (int g = 0; g < 16; ++g)
+          v[g] = g < G ? __ldcg(p.zpart + (static_cast<int64_t>(g) * p.zpad + row) * EP + e) : 0.f;
+#pragma unroll
+        for (int g = 0; g < 16; ++g)
+          if (g < G) acc += v[g];
+      }
+      if (e < E) {
+        acc += __ldg(p.b2 + e);
+        bad |= !isfinite(acc);
+      } else {
+        acc = -INFINITY;
+      }
+      zv[q] = acc;
+    }
     float sumsq = 0.f;
-    if (valid) {
-      for (int g = 0; g < G; ++g) {
-        const float4* zp = reinterpret_cast<const float4*>(p.zpart + (static_cast<int64_t>(g) * p.zpad + row) * EP);
+    {
+      // lane g loads group g's ||h||^2 partial; lane 0 sums them in order
+      const float part = lane < G ? __ldcg(sq + static_cast<int64_t>(lane) * p.zpad + row) : 0.f;
 #pragma unroll
-        for (int j = 0; j < EP / 4; ++j) {
-          const float4 v = __ldcg(zp + j);
-          z[4 * j] += v.x; z[4 * j + 1] += v.y; z[4 * j + 2] += v.z; z[4 * j + 3] += v.w;
-        }
-        sumsq += __ldcg(sq + static_cast<int64_t>(g) * p.zpad + row);
+      for (int g = 0; g < 16; ++g) {
+        const float v = __shfl_sync(0xffffffffu, part, g);
+        if (g < G) sumsq += v;
       }
     }
-    k1c::row_epilogue<EP>(p, z, sumsq, row, valid, lane, hist, rc, zrow, zswz);
+    bool flagged = __any_sync(0xffffffffu, bad);
+    // sorted top list (warp-uniform): repeated warp argmax over the untaken experts
+    float tv[kMaxSel];
+    int tix[kMaxSel];
+    uint32_t taken = 0;
+#pragma unroll
+    for (int s = 0; s < kMaxSel; ++s) {
+      float best = -INFINITY;
+      int bi = 0x7fffffff;
+      if (s < P) {
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+          const int e = q * 32 + lane;
+          if (!((taken >> q) & 1u) && e < EP && (zv[q] > best || (zv[q] == best && e < bi))) { best = zv[q]; bi = e; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+        }
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+      }
+      tv[s] = best;
+      tix[s] = bi;
+    }
+    const float delta = p.tau_abs + p.tau_rel * sqrtf(sumsq) * p.w2_norm;
+#pragma unroll
+    for (int b = 0; b < MOEP_MAX_BOUNDS; ++b) {
+      if (b < p.n_bounds) {
+        const int pos = p.bounds[b];
+        if (pos >= 1 && pos < E) {
+          float hi_v = tv[0], lo_v = tv[1];
+#pragma unroll
+          for (int s = 1; s < kMaxSel; ++s)
+            if (s == pos) { hi_v = tv[s - 1]; lo_v = tv[s]; }
+          flagged |= !(hi_v - lo_v >= delta);
+        }
+      }
+    }
+    if (lane == 0) {
+      if (p.flags) p.flags[row] = flagged ? 1 : 0;
+      if (flagged) p.flag_list[atomicAdd(p.flag_count, 1)] = static_cast<int>(row);
+    }
+    if (p.logits) {
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const int e = q * 32 + lane;
+        if (e < E) p.logits[row * E + e] = zv[q];
+      }
+    }
+    if (p.ids && !flagged) {
+      int* orow = p.ids + row * p.m_sel;
+      if (p.m_sel >= E) {
+        for (int e = lane; e < E; e += 32) orow[e] = e;
+      } else {
+        float thv = tv[0];
+        int thi = tix[0];
+#pragma unroll
+        for (int s = 0; s < kMaxSel; ++s)
+          if (s == p.m_sel - 1) { thv = tv[s]; thi = tix[s]; }
+        int base = 0;
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+          const int e = q * 32 + lane;
+          const bool sel = e < E && ((zv[q] > thv || (zv[q] == thv && e < thi)) || e == thi);
+          const uint32_t mask = __ballot_sync(0xffffffffu, sel);
+          if (sel) orow[base + __popc(mask & ((1u << lane) - 1u))] = e;
+          base += __popc(mask);
+        }
+      }
+    }
+    if (p.truth && !flagged) {
+      // "truth expert t has predicted rank < m" <=> key(t) >= key(position m-1) of the top list
+      const bool act = lane < p.k;
+      const int t = act ? __ldg(p.truth + row * p.k + lane) : 0;
+      float zt = 0.f;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const float v = __shfl_sync(0xffffffffu, zv[q], t & 31);
+        if ((t >> 5) == q) zt = v;
+      }
+      auto thr = [&](int m, float& v, int& ix) {
+        v = tv[0];
+        ix = tix[0];
+#pragma unroll
+        for (int s = 0; s < kMaxSel; ++s)
+          if (s == m - 1) { v = tv[s]; ix = tix[s]; }
+      };
+      float kv;
+      int ki;
+      thr(p.k, kv, ki);
+      const bool hit = act && ((zt > kv || (zt == kv && t < ki)) || t == ki);
+      if (act) {
+        atomicAdd(&hist_s[EP + t], 1);
+        if (hit) atomicAdd(&hist_s[t], 1);
+      }
+      const bool any0 = __any_sync(0xffffffffu, act && t == tix[0]);
+      rc.n += 1;
+      rc.top1 += any0 ? 1 : 0;
+#pragma unroll
+      for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
+        if (mi < p.n_m) {
+          const int m = p.m_list[mi];
+          float mv;
+          int mx;
+          thr(m < kMaxSel ? m : 1, mv, mx);
+          const bool in = act && (m >= E || (zt > mv || (zt == mv && t < mx)) || t == mx);
+          const int cnt = __popc(__ballot_sync(0xffffffffu, in));
+          rc.ov[mi] += cnt == p.k ? 1 : 0;
+          rc.rc[mi] += cnt;
+        }
+      }
+    }
   }
-  if (p.partials) k1c::write_partials<EP>(p, rc, q, lane, tid, red0, hist0, 1);
+  if (p.partials) {
+    if (lane == 0) {
+      atomicAdd(&cnt_s[0], rc.n);
+      atomicAdd(&cnt_s[1], rc.top1);
+#pragma unroll
+      for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
+        atomicAdd(&cnt_s[2 + mi], rc.ov[mi]);
+        atomicAdd(&cnt_s[2 + MOEP_MAX_BOUNDS + mi], rc.rc[mi]);
+      }
+    }
+    __syncthreads();
+    int* out = p.partials + static_cast<int64_t>(blockIdx.x) * p.n_counters;
+    for (int t = tid; t < p.n_counters; t += 256) {
+      int v;
+      if (t < 2) v = cnt_s[t];
+      else if (t < 2 + p.n_m) v = cnt_s[2 + (t - 2)];
+      else if (t < 2 + 2 * p.n_m) v = cnt_s[2 + MOEP_MAX_BOUNDS + (t - 2 - p.n_m)];
+      else {
+        const int u = t - 2 - 2 * p.n_m;  // [hits E | truth E]
+        v = u < E ? hist_s[u] : hist_s[EP + (u - E)];
+      }
+      out[t] = v;
+    }
+  }
 }
 
 // Chunk groups per tile: only when the tiles leave CTA pairs idle (fewer tiles
@@ -410,14 +568,17 @@ static int choose_split(int64_t n_tokens, int hidden, int n_pairs) {
   const int nchunks = hidden / HC;
   const int64_t tiles = (n_tokens + 2 * BM - 1) / (2 * BM);
   if (tiles >= n_pairs) return 1;
+  const int64_t cost1 = ((tiles + n_pairs - 1) / n_pairs) * nchunks;
   int best = 1;
-  int64_t best_cost = ((tiles + n_pairs - 1) / n_pairs) * nchunks;
+  int64_t best_cost = cost1;
   for (int g = 2; g <= nchunks && g <= 16; g *= 2) {
     if (nchunks % g) continue;
     const int64_t cost = ((tiles * g + n_pairs - 1) / n_pairs) * (nchunks / g);
     if (cost < best_cost) { best = g; best_cost = cost; }
   }
-  return best;
+  // a split pays per-item pipeline fills, the partial-logit traffic and the
+  // finish kernel: take it only for a clear gain (at most 3/4 of the rounds)
+  return 4 * best_cost <= 3 * cost1 ? best : 1;
 }
 
 }  // namespace k1v2
@@ -474,12 +635,7 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
   kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);
   if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
   if (p.split > 1) {
-    auto fin = split_finish_kernel<EP>;
-    const int fsmem = 4 * 2 * EP * 4 + 64 * 4 + 128 * (EP + 1) * 4;
-    if (fsmem > 48 * 1024 &&
-        cudaFuncSetAttribute(fin, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem) != cudaSuccess)
-      return MOEP_ELAUNCH;
-    fin<<<moep_num_sms(), 128, fsmem, st>>>(p);
+    split_finish_kernel<EP><<<moep_num_sms(), 256, 0, st>>>(p);
     if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
   }
   return MOEP_OK;
