@@ -277,3 +277,52 @@ def test_fixup_overflow_path(pb, O, tau_rel, lo, hi):
         assert c.top1 == oc["top1_count"] and np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
         z = dev.logits(xt).cpu().numpy()
         assert np.abs(z - zref).max() < LOGIT_ATOL_K1
+
+
+# ------------------------------------------------ shape / argument edge cases
+EDGE = [
+    # arch, d, h, E, k, n, ms        why
+    ("arch2", 512, 512, 48, 6, 2000, (6, 10, 48)),     # E not a power of two (EP = 64 padding)
+    ("arch2", 256, 384, 32, 4, 1500, (4, 8, 32)),      # hidden % 256 != 0 -> 1-SM kernel
+    ("arch2", 512, 512, 64, 16, 1200, (15, 16, 64)),   # k = 16 (max truth) and m = 15 (max selection)
+    ("arch1", 512, 512, 64, 6, 700, (6, 10, 64)),      # arch1 through the hidden split (small N)
+    ("arch2", 136, 256, 16, 2, 333, (2, 6, 16)),       # d not a multiple of 64 (TMA tail K block)
+]
+
+
+@pytest.mark.parametrize("arch,d,h,e,k,n,ms", EDGE)
+def test_edge_shapes_vs_oracle(pb, O, arch, d, h, e, k, n, ms):
+    rng = np.random.default_rng(d + h + e + n)
+    m = bf16_model(pb, O, arch, d, h, e, seed=11, rng=rng)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref = O.predict_logits(oracle_params(m), x)
+    dev = m.to_device()
+    dev.decode_max_tokens = 0
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    for mm in sorted({1, min(k, 15), 15 if e > 15 else e, e}):
+        assert np.array_equal(dev.topk(xt, mm).cpu().numpy(), O.top_k_batch(zref, mm)), mm
+    truth = O.top_k_batch(zref + 0.05 * rng.standard_normal(zref.shape), k)
+    cnt, _, ids = dev.evaluate(xt, torch.from_numpy(truth), k, list(ms), ids_m=min(k, 15))
+    c = pb.EvalCounters.from_array(cnt.cpu().numpy(), k, e, sorted(set(ms) | {k}))
+    oc = O.eval_counters(zref, truth, e, list(ms))
+    assert c.n == n and c.top1 == oc["top1_count"]
+    assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
+    assert np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
+    assert np.array_equal(c.per_expert_truth, oc["per_expert_truth"])
+    assert np.array_equal(ids.cpu().numpy(), O.top_k_batch(zref, min(k, 15)))
+
+
+def test_ties_through_hidden_split_and_decode(pb, O):
+    """Exact ties (duplicated W2 rows) on the split-hidden tensor path (N=300) and
+    the decode path (N=5): lower index wins, as core.py:27-48."""
+    rng = np.random.default_rng(8)
+    m = bf16_model(pb, O, "arch2", 512, 512, 16, seed=4)
+    m.w2[7] = m.w2[3]
+    m.w2[12] = m.w2[3]
+    for n in (300, 5):
+        x = O.round_bf16(rng.standard_normal((n, 512)))
+        zref = O.predict_logits(oracle_params(m), x)
+        dev = m.to_device()
+        xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+        for mm in (1, 2, 3, 5):
+            assert np.array_equal(dev.topk(xt, mm).cpu().numpy(), O.top_k_batch(zref, mm)), (n, mm)
