@@ -142,16 +142,19 @@ def _round_bf16_np(a):
     return np.ldexp(np.rint(m * 256.0), e - 8)
 
 
-def step(layers, k1_events=None):
-    """One pass over every layer: fused predict + eval (K1), fp64 fix-up (K2), reduce."""
+def step(layers, k1_events=None, layer_events=None):
+    """One pass over every layer: fused predict + eval (K1), fp64 fix-up (K2), reduce.
+    k1_events[li]: (start, end) around the K1 launch alone; layer_events[li]:
+    around the whole per-layer pipeline (both on the launching stream)."""
     outs = []
     for li, (_, dp, x, truth) in enumerate(layers):
         prepared = (x, x, True)
-        if k1_events is not None:
-            k1_events[li][0].record()
-        cnt, fcount, _ = dp.evaluate(x, truth, K_ACT, M_LIST, prepared=prepared)
-        if k1_events is not None:
-            k1_events[li][1].record()
+        if layer_events is not None:
+            layer_events[li][0].record()
+        cnt, fcount, _ = dp.evaluate(x, truth, K_ACT, M_LIST, prepared=prepared,
+                                     k1_events=None if k1_events is None else k1_events[li])
+        if layer_events is not None:
+            layer_events[li][1].record()
         outs.append((cnt, fcount))
     return outs
 
@@ -201,6 +204,8 @@ def main():
     # ---- timed region: device events around K steps, barrier + sync on both sides
     k1_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.layers)] for _ in range(args.steps)]
+    lay_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.layers)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -208,7 +213,7 @@ def main():
     with ClockSampler(local_rank) as clk:
         start.record()
         for s in range(args.steps):
-            flat = all_reduce_counters(step(layers, k1_ev[s]))
+            flat = all_reduce_counters(step(layers, k1_ev[s], lay_ev[s]))
         stop.record()
         torch.cuda.synchronize()
     if world > 1:
@@ -221,9 +226,9 @@ def main():
     ms_step = ms_total / args.steps
     value = world * n_tok_rank * args.steps / (ms_total / 1e3)
 
-    # per-launch time of the evaluate pipeline (K1 dominant) inside the timed region
-    per_layer_ms = [a.elapsed_time(b) for row in k1_ev for (a, b) in row]
-    pipe_ms = statistics.mean(per_layer_ms)
+    # inside the timed region: per-layer pipeline time and the K1 launch alone
+    pipe_ms = statistics.mean([a.elapsed_time(b) for row in lay_ev for (a, b) in row])
+    k1_ms = statistics.mean([a.elapsed_time(b) for row in k1_ev for (a, b) in row])
 
     # counters of the last step (for the accuracy line and the flagged fraction)
     import paper_2511_10676_b200 as pb
@@ -232,8 +237,8 @@ def main():
     flagged = int(flat_np[args.layers * ncnt:].sum())
     c0 = pb.EvalCounters.from_array(flat_np[:ncnt], K_ACT, E, M_LIST)
 
-    # K1 alone (same stream, events) for the roofline: time one layer's K1 launch
-    k1_ms = time_k1(layers[0][1], layers[0][2], layers[0][3], reps=5)
+    # K1 alone outside the timed region (5 back-to-back launches), for reference
+    k1_ms_standalone = time_k1(layers[0][1], layers[0][2], layers[0][3], reps=5)
     burst, sustained, hbm, src = peaks()
     achieved_tflops = FLOP_PER_TOKEN * args.tokens / (k1_ms / 1e3) / 1e12
 
@@ -271,7 +276,9 @@ def main():
                          "frac": achieved_tflops / sustained, "peak_kind": f"{src} sustained bf16",
                          "frac_of_burst": achieved_tflops / burst, "kernel": "moep k1 predict_kernel",
                          "flop_per_token": FLOP_PER_TOKEN, "tokens_per_launch": args.tokens,
-                         "k1_ms_per_launch": k1_ms, "pipeline_ms_per_layer": pipe_ms,
+                         "k1_ms_per_launch": k1_ms, "k1_timing": "CUDA events around every K1 launch "
+                                                                "inside the timed region, mean",
+                         "k1_ms_standalone": k1_ms_standalone, "pipeline_ms_per_layer": pipe_ms,
                          "traffic": _k1_traffic(args.tokens),
                          "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch, "
                                            "ncu --set full (profiles/r01_k1_traffic.json), scaled to tokens"},

@@ -326,8 +326,11 @@ class DevicePredictor:
         return (ids, flags) if return_flags else ids
 
     def evaluate(self, x: torch.Tensor, truth: torch.Tensor, k: int, m_values, ids_m: int = 0,
-                 prepared=None) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+                 prepared=None, k1_events=None) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
         """Fused predict + evaluation counters on device.
+
+        k1_events: optional (start, end) CUDA events recorded on the current
+        stream around the fused tensor-core kernel alone (profiling hook).
 
         Returns (counters int64 [n_counters], flag_count int32 [1], ids or None)
         without synchronising; see EvalCounters.from_array for the layout.
@@ -360,8 +363,12 @@ class DevicePredictor:
         bounds = tuple(p for p in positions if p < self.E)
         if len(m_values) <= _lib.MAX_BOUNDS and len(bounds) <= _lib.MAX_BOUNDS and self.k1_usable(exact, bounds) \
                 and k <= 16:
+            if k1_events is not None:
+                k1_events[0].record()
             flags, flist, fcount = self._k1(xb, m_sel=ids_m, bounds=bounds, ids=ids, truth=truth, k=k,
                                             m_values=m_values, partials=partials[: self.n_sms])
+            if k1_events is not None:
+                k1_events[1].record()
             a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, m_sel=ids_m, ids=ids,
                                 truth=truth, k=k, m_values=m_values,
                                 partials=partials[self.n_sms: 2 * self.n_sms])
