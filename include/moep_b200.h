@@ -265,6 +265,20 @@ int moep_bn_backward(const double* dz, const double* w2, int64_t n, int32_t hidd
                      const double* inv_std, const double* scale, double* da, double* dw2, double* db1,
                      double* dscale, double* dshift, int32_t training, void* stream);
 
+/* ----------------------------------------------------------------- K10 --
+ * MOEPA1 trace records -> device arrays (synthgen.py:219-253 read_trace,
+ * record invariants :123-145 TraceFile.validate). `records` holds n raw
+ * little-endian records [d x f32 | E x f32 | k x u32] in device memory;
+ * rows row0 .. row0+n-1 of acts ([*, d], fp32 or bf16 per act_dtype), scores
+ * ([*, E] fp32) and topk ([*, k] int32) are written. status[6] (device,
+ * caller-zeroed, accumulated across calls) counts failing records per check,
+ * in the reference's order: non-finite activation, score outside [0, 1],
+ * scores not summing to 1 within 1e-5, index >= E, row not strictly
+ * increasing, stored top-k != top_k(scores, k). */
+int moep_trace_ingest(const uint32_t* records, int64_t n, int32_t d, int32_t n_experts, int32_t k,
+                      int32_t act_dtype, void* acts, float* scores, int32_t* topk, int64_t row0,
+                      unsigned long long* status, void* stream);
+
 /* ------------------------------------------------------------ prefetch --
  * K8: union of the predicted expert ids of a batch (ids[0 .. n_ids)), minus
  * experts already resident (slot_of[e] >= 0; NULL = none resident): ascending

@@ -91,6 +91,7 @@ _SIGS = {
     "moep_bn_backward": [vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp],
     "moep_prefetch_plan": [vp, i64, i32, vp, vp, i32, vp, vp, vp, vp, vp],
     "moep_gather_experts": [vp, i64, vp, vp, vp, vp, i32, vp],
+    "moep_trace_ingest": [vp, i64, i32, i32, i32, i32, vp, vp, vp, i64, vp, vp],
     "moep_num_sms": [],
     "moep_version": [],
 }

@@ -19,6 +19,9 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from moepredict import core, losses, metrics, predictor  # noqa: E402
 from moepredict.trainer import TrainConfig, _Optimizer  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from trace_corrupt import corruptions as _corruptions  # noqa: E402
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
@@ -149,12 +152,64 @@ def adam_cases():
     return out
 
 
+def trace_cases():
+    """MOEPA1 files written / read by the reference (synthgen.py:197-253)."""
+    import tempfile
+    from moepredict import synthgen, exceptions
+    rng = np.random.default_rng(7)
+    d, e, k = 32, 16, 4
+    router = core.RouterSpec(d, e, k, rng.standard_normal((e, d)) / np.sqrt(d))
+    teacher = synthgen.TeacherSpec(router, transform="nonlinear", noise_sigma=0.1, seed=5)
+    data = synthgen.generate_dataset(teacher, 200)
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "t.moepa")
+        synthgen.write_trace(path, data)
+        blob = open(path, "rb").read()
+        with open(os.path.join(HERE, "trace_small.moepa"), "wb") as f:
+            f.write(blob)
+        back = synthgen.read_trace(path)
+        out["acts"], out["scores"], out["topk"] = back.activations, back.true_scores, back.true_topk
+        out["dims"] = np.array([d, e, k, len(back)])
+        # ties: scores with exact equal values (lower index must win)
+        sc = np.zeros((64, 8), dtype=np.float64)
+        sc[:, :4] = 0.25
+        sc[32:] = rng.dirichlet(np.ones(8), size=32)
+        sc[40:48, 2] = sc[40:48, 5]
+        sc = sc / sc.sum(axis=1, keepdims=True)
+        tie = synthgen.make_dataset(rng.standard_normal((64, 8)), sc, 3)
+        synthgen.write_trace(path, tie)
+        with open(os.path.join(HERE, "trace_ties.moepa"), "wb") as f:
+            f.write(open(path, "rb").read())
+        out["tie_topk"] = synthgen.read_trace(path).true_topk
+        # corruptions: the exception class the reference raises for each
+        names, kinds, msgs = [], [], []
+        for name, bad in _corruptions(blob, d, e, k).items():
+            with open(path, "wb") as f:
+                f.write(bad)
+            try:
+                synthgen.read_trace(path)
+                kind = "ok"
+            except exceptions.MoePredictError as exc:
+                kind = type(exc).__name__
+                msgs.append(str(exc))
+            else:
+                msgs.append("")
+            names.append(name)
+            kinds.append(kind)
+        out["corrupt_names"] = np.array(names)
+        out["corrupt_kinds"] = np.array(kinds)
+        out["corrupt_msgs"] = np.array(msgs)
+    return out
+
+
 def main():
     np.savez_compressed(os.path.join(HERE, "topk.npz"), **topk_cases())
     np.savez_compressed(os.path.join(HERE, "predictor.npz"), **predictor_cases())
     np.savez_compressed(os.path.join(HERE, "losses.npz"), **loss_cases())
     np.savez_compressed(os.path.join(HERE, "metrics.npz"), **metric_cases())
     np.savez_compressed(os.path.join(HERE, "optim.npz"), **adam_cases())
+    np.savez_compressed(os.path.join(HERE, "trace.npz"), **trace_cases())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -5,6 +5,8 @@
     (tests/golden/make_golden.py).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -200,3 +202,34 @@ def test_oracle_gradients_fd(rng):
             fd = central_diff(lambda: O.loss_and_grad(spec, O.predict_logits(p, x), lab)[0], params)
             for name in params:
                 assert rel_error(grads[name], fd[name]) < 1e-4, (arch, fam, name)
+
+
+# ------------------------------------------------------------ MOEPA1 traces
+def _trace_golden():
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    g = np.load(os.path.join(here, "trace.npz"))
+    blob = open(os.path.join(here, "trace_small.moepa"), "rb").read()
+    ties = open(os.path.join(here, "trace_ties.moepa"), "rb").read()
+    return g, blob, ties
+
+
+def test_oracle_trace_reads_reference_files():
+    from oracle import trace as T
+    g, blob, ties = _trace_golden()
+    d, e, k, acts, scores, topk = T.read_trace(blob)
+    assert [d, e, k, len(acts)] == g["dims"].tolist()
+    assert np.array_equal(acts, g["acts"]) and np.array_equal(scores, g["scores"])
+    assert np.array_equal(topk, g["topk"])
+    assert np.array_equal(T.read_trace(ties)[5], g["tie_topk"])
+
+
+def test_oracle_trace_corruptions_match_reference_exceptions():
+    from trace_corrupt import corruptions
+    from oracle import trace as T
+    g, blob, _ = _trace_golden()
+    d, e, k, _n = g["dims"].tolist()
+    bad = corruptions(blob, d, e, k)
+    for name, kind, msg in zip(g["corrupt_names"], g["corrupt_kinds"], g["corrupt_msgs"]):
+        with pytest.raises(T.OracleTraceError) as ei:
+            T.read_trace(bad[str(name)])
+        assert ei.value.kind == kind and str(ei.value) == msg, name
