@@ -14,7 +14,8 @@ import os
 from .exceptions import ConfigurationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmoep_b200.so")
+# MOEP_LIB: alternative build of the same library (the profiling build of tools/k1_prof.py)
+LIB_PATH = os.environ.get("MOEP_LIB") or os.path.join(_HERE, "libmoep_b200.so")
 
 MOEP_OK, MOEP_ESHAPE, MOEP_EALIGN, MOEP_EUNSUPPORTED, MOEP_ELAUNCH, MOEP_EARG = 0, -1, -2, -3, -4, -5
 MOEP_BF16, MOEP_F64, MOEP_F32 = 1, 2, 3

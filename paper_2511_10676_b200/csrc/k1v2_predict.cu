@@ -32,6 +32,21 @@ namespace k1v2 {
 using k1c::Params;
 using k1c::wait;
 
+// Role-level wait accounting for tools/k1_prof.py, compiled only with
+// -DMOEP_K1_PROF (a separate library; the product build has no counters):
+// cycles spent in each barrier wait by one representative thread per role.
+#ifdef MOEP_K1_PROF
+__device__ unsigned long long g_k1_prof[160][16];
+#define K1_PW(slot, rep, call)                                                         \
+  do {                                                                                 \
+    const long long t0_ = clock64();                                                   \
+    call;                                                                              \
+    if (rep) atomicAdd(&g_k1_prof[blockIdx.x][slot], (unsigned long long)(clock64() - t0_)); \
+  } while (0)
+#else
+#define K1_PW(slot, rep, call) call
+#endif
+
 constexpr int BM = 128;         // tokens per CTA (256 per pair)
 constexpr int BK = 64;          // K per stage
 constexpr int HC = 256;         // hidden columns per chunk (pair MMA N)
@@ -82,6 +97,9 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
   uint64_t* z_empty = z_full + 1;             // leader: 8 warps read z
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
+#ifdef MOEP_K1_PROF
+  const long long k1_t_start = clock64();
+#endif
   const uint32_t warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -128,7 +146,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
           for (int c = c0; c < c0 + cpg; ++c) {
             const int wrow = c * HC + rank * HB;
             for (int kb = 0; kb < nk; ++kb) {
-              wait(&empty[stage], phase ^ 1);
+              K1_PW(0, true, wait(&empty[stage], phase ^ 1));
               if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
               tma_load_2d_cg2(&tm_x, &full[stage], smem + C::OFF_A + stage * C::A_BYTES, kb * BK, xrow, keep);
               tma_load_2d_cg2(&tm_w1, &full[stage], smem + C::OFF_B + stage * C::B_BYTES, kb * BK, wrow, keep);
@@ -145,7 +163,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         for (int item = pair; item < n_items; item += n_pairs) {
           const int c0 = (item % G) * cpg;
           for (int c = c0; c < c0 + cpg; ++c, ++n) {
-            if (n > 0) wait(w2_empty, (n - 1) & 1);
+            if (n > 0) K1_PW(1, true, wait(w2_empty, (n - 1) & 1));
             if (leader) mbar_arrive_expect_tx(w2_full, 2 * 4 * C::W2_ATOM);
 #pragma unroll
             for (int at = 0; at < 4; ++at)
@@ -172,13 +190,13 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
           while (p_half < 2) {
             if (p_half == 0) {
               if (p_cc == 0) {
-                if (block) wait(z_empty, (p_ti & 1) ^ 1);
+                if (block) K1_PW(2, true, wait(z_empty, (p_ti & 1) ^ 1));
                 else if (!k1c::test(z_empty, (p_ti & 1) ^ 1)) return;
               }
-              if (block) wait(w2_full, p_id & 1);
+              if (block) K1_PW(3, true, wait(w2_full, p_id & 1));
               else if (!k1c::test(w2_full, p_id & 1)) return;
             }
-            if (block) wait(&a2_full[p_half], p_id & 1);
+            if (block) K1_PW(4, true, wait(&a2_full[p_half], p_id & 1));
             else if (!k1c::test(&a2_full[p_half], p_id & 1)) return;
             tc_fence_after();
             const int half = p_half;
@@ -203,10 +221,10 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         };
         for (int item = pair; item < n_items; item += n_pairs, ++ti) {
           for (int c = 0; c < cpg; ++c, ++gc) {  // c: chunk within the item
-            wait(acc_empty, (gc & 1) ^ 1);
+            K1_PW(5, true, wait(acc_empty, (gc & 1) ^ 1));
             tc_fence_after();
             for (int kb = 0; kb < nk; ++kb) {
-              wait(&full[stage], phase);
+              K1_PW(6, true, wait(&full[stage], phase));
               tc_fence_after();
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k) {
@@ -245,7 +263,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       const int64_t row_g = static_cast<int64_t>(tile) * 2 * BM + rank * BM + row_in_tile;
       float sumsq = 0.f;
       for (int c = c0; c < c0 + cpg; ++c, ++gc) {
-        wait(acc_full, gc & 1);
+        K1_PW(wg == 0 ? 7 : 11, lane == 0 && q == 0, wait(acc_full, gc & 1));
         tc_fence_after();
         float v[128];
         const uint32_t ta = tmem + lane_addr + wg * 128;
@@ -295,9 +313,9 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         }
         // the A2 buffer is free once the previous GEMM2 half that read it completed
         if (wg == 0) {
-          if (gc > 0) wait(a2_emptyB, (gc - 1) & 1);
+          if (gc > 0) K1_PW(8, lane == 0 && q == 0, wait(a2_emptyB, (gc - 1) & 1));
         } else {
-          wait(a2_emptyA, gc & 1);
+          K1_PW(9, lane == 0 && q == 0, wait(a2_emptyA, gc & 1));
         }
         uint8_t* a2hi = smem + C::OFF_A2;
         uint8_t* a2lo = smem + C::OFF_A2 + 2 * C::ATOM;
@@ -324,7 +342,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (wg == 0) {
         sumsq += s_sumsq[row_in_tile];
-        wait(z_full, ti & 1);
+        K1_PW(10, lane == 0 && q == 0, wait(z_full, ti & 1));
         tc_fence_after();
         float z[EP];
 #pragma unroll
@@ -354,6 +372,9 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
   }
   tc_fence_before();
   __syncthreads();
+#ifdef MOEP_K1_PROF
+  if (threadIdx.x == 0) atomicAdd(&g_k1_prof[blockIdx.x][15], (unsigned long long)(clock64() - k1_t_start));
+#endif
   cluster_sync();
   if (warp == 3) tmem_dealloc_cg2<512>(tmem);
 }
@@ -583,6 +604,17 @@ static int choose_split(int64_t n_tokens, int hidden, int n_pairs) {
 
 }  // namespace k1v2
 }  // namespace moep
+
+#ifdef MOEP_K1_PROF
+extern "C" int moep_k1_prof(unsigned long long* host, int reset) {
+  if (reset) {
+    static unsigned long long zero[160][16];
+    return cudaMemcpyToSymbol(moep::k1v2::g_k1_prof, zero, sizeof(zero)) == cudaSuccess ? 0 : -4;
+  }
+  return cudaMemcpyFromSymbol(host, moep::k1v2::g_k1_prof, sizeof(unsigned long long) * 160 * 16) == cudaSuccess
+             ? 0 : -4;
+}
+#endif
 
 extern "C" int64_t moep_predict_split_floats(int64_t n_tokens, int32_t hidden, int32_t n_experts) {
   using namespace moep::k1v2;
