@@ -264,6 +264,9 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       float sumsq = 0.f;
       for (int c = c0; c < c0 + cpg; ++c, ++gc) {
         K1_PW(wg == 0 ? 7 : 11, lane == 0 && q == 0, wait(acc_full, gc & 1));
+#ifdef MOEP_K1_PROF
+        const long long t_drain0 = clock64();
+#endif
         tc_fence_after();
         float v[128];
         const uint32_t ta = tmem + lane_addr + wg * 128;
@@ -275,6 +278,11 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(acc_empty, 0);
+#ifdef MOEP_K1_PROF
+        if (lane == 0 && q == 0)
+          atomicAdd(&g_k1_prof[blockIdx.x][wg == 0 ? 12 : 13], (unsigned long long)(clock64() - t_drain0));
+        const long long t_conv0 = clock64();
+#endif
         // bias + activation + hi/lo split, in place per column pair (2j, 2j+1):
         // v[2j] <- packed bf16x2 hi, v[2j+1] <- packed bf16x2 lo
         const int col0 = c * HC + wg * 128;
@@ -289,7 +297,13 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
               *reinterpret_cast<float4*>(p.a_out + row_g * p.hidden + col) =
                   make_float4(v[j4 * 4] + bv[0], v[j4 * 4 + 1] + bv[1], v[j4 * 4 + 2] + bv[2], v[j4 * 4 + 3] + bv[3]);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) hv[t] = silu_f32(v[j4 * 4 + t] + bv[t]);
+            for (int t = 0; t < 4; ++t) {
+#ifdef MOEP_K1_PROF_NOACT  // timing experiment only (tools/k1_prof.py --noact): identity activation
+              hv[t] = v[j4 * 4 + t] + bv[t];
+#else
+              hv[t] = silu_f32(v[j4 * 4 + t] + bv[t]);
+#endif
+            }
           } else {
             const float4 aa = __ldg(reinterpret_cast<const float4*>(p.alpha + col));
             const float4 bb = __ldg(reinterpret_cast<const float4*>(p.beta + col));
@@ -301,16 +315,19 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
           for (int t = 0; t < 4; t += 2) {
             sumsq = fmaf(hv[t], hv[t], sumsq);
             sumsq = fmaf(hv[t + 1], hv[t + 1], sumsq);
-            const __nv_bfloat16 h0 = __float2bfloat16_rn(hv[t]);
-            const __nv_bfloat16 h1 = __float2bfloat16_rn(hv[t + 1]);
-            const __nv_bfloat16 l0 = __float2bfloat16_rn(hv[t] - __bfloat162float(h0));
-            const __nv_bfloat16 l1 = __float2bfloat16_rn(hv[t + 1] - __bfloat162float(h1));
-            v[j4 * 4 + t] = __uint_as_float(static_cast<uint32_t>(__bfloat16_as_ushort(h0)) |
-                                            (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16));
-            v[j4 * 4 + t + 1] = __uint_as_float(static_cast<uint32_t>(__bfloat16_as_ushort(l0)) |
-                                                (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16));
+            // packed conversions (one F2FP per column pair): hi = bf16x2(h), lo = bf16x2(h - hi);
+            // column t in the low half, as the swizzled A2 layout expects
+            const __nv_bfloat162 hp = __floats2bfloat162_rn(hv[t], hv[t + 1]);
+            const float2 hf = __bfloat1622float2(hp);
+            const __nv_bfloat162 lp = __floats2bfloat162_rn(hv[t] - hf.x, hv[t + 1] - hf.y);
+            v[j4 * 4 + t] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&hp));
+            v[j4 * 4 + t + 1] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&lp));
           }
         }
+#ifdef MOEP_K1_PROF
+        if (lane == 0 && q == 0) atomicAdd(&g_k1_prof[blockIdx.x][wg == 0 ? 14 : 3], 0ull);
+        if (lane == 0 && q == 0 && wg == 0) atomicAdd(&g_k1_prof[blockIdx.x][14], (unsigned long long)(clock64() - t_conv0));
+#endif
         // the A2 buffer is free once the previous GEMM2 half that read it completed
         if (wg == 0) {
           if (gc > 0) K1_PW(8, lane == 0 && q == 0, wait(a2_emptyB, (gc - 1) & 1));

@@ -12,14 +12,20 @@ OUT = os.path.join(ROOT, "tools", "_k1prof")
 LIB = os.path.join(OUT, "libmoep_b200_prof.so")
 
 
+NOACT = "--noact" in sys.argv
+if NOACT:
+    LIB = os.path.join(OUT, "libmoep_b200_prof_noact.so")
+
+
 def build():
     sys.path.insert(0, ROOT)
     from paper_2511_10676_b200 import build as b
     os.makedirs(OUT, exist_ok=True)
     objs = []
     for src in b.sources():
-        obj = os.path.join(OUT, os.path.basename(src).replace(".cu", ".o"))
+        obj = os.path.join(OUT, os.path.basename(src).replace(".cu", "_noact.o" if NOACT else ".o"))
         subprocess.run([b.nvcc(), *b.ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-DMOEP_K1_PROF",
+                        *(["-DMOEP_K1_PROF_NOACT"] if NOACT else []),
                         "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj], check=True)
         objs.append(obj)
     subprocess.run([b.nvcc(), *b.ARCH, "-shared", "-o", LIB, *objs], check=True)
@@ -54,9 +60,10 @@ if __name__ == "__main__":
              3: "MMA: wait w2_full", 4: "MMA: wait a2_full (block)", 5: "MMA: wait acc_empty",
              6: "MMA: wait full (operands)", 7: "EPI WG0: wait acc_full", 8: "EPI WG0: wait a2_emptyB",
              9: "EPI WG1: wait a2_emptyA", 10: "EPI WG0: wait z_full", 11: "EPI WG1: wait acc_full",
-             15: "total kernel cycles (thread 0)"}
+             12: "EPI WG0: drain (ld + arrive) duration", 13: "EPI WG1: drain duration",
+             14: "EPI WG0: bias/act/hi-lo convert duration", 15: "total kernel cycles (thread 0)"}
     lead = buf[0:148:2]          # leader CTAs (MMA issuer lives there)
     tot = lead[:, 15].astype(float).mean()
     for s_, n in names.items():
         v = lead[:, s_].astype(float).mean()
-        print(f"{n:40s} {v / tot * 100:6.2f} %  ({v:.0f} cycles)")
+        print(f"{n:44s} {v / tot * 100:6.2f} %  ({v:.0f} cycles, {v / 448:.0f} per chunk)")
