@@ -549,7 +549,10 @@ extern "C" int moep_predict_bf16(const moep_predict_args* a, void* stream) {
     const char* env = getenv("MOEP_K1_VARIANT");
     variant = (env && env[0] == '1') ? 1 : 2;
   }
-  if (variant == 2 && a->hidden % 256 == 0) return moep_predict_bf16_pair(a, stream);
+  if (variant == 2) {
+    const int rc = moep_predict_bf16_pair(a, stream);
+    if (rc != MOEP_EUNSUPPORTED) return rc;
+  }
   int EP = 16;
   while (EP < a->n_experts) EP *= 2;
   CUtensorMap tx, tw1, tw2;

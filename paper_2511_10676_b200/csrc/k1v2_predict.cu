@@ -598,18 +598,35 @@ __global__ void __launch_bounds__(256) split_finish_kernel(const Params p) {
   }
 }
 
+// Which pair kernel runs: v2 (256-column chunks, single accumulator) by
+// default; MOEP_K1_VARIANT=3 selects v3 (double-buffered accumulator,
+// 192-column chunks, E <= 64), which removes the drain bubble but measured
+// slower (the per-chunk epilogue becomes the limit: profiles/r01_k1_role_waits.md).
+// MOEP_K1_VARIANT=1 selects the 1-SM kernel in moep_predict_bf16.
+static bool use_v3(int hidden, int n_experts) {
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("MOEP_K1_VARIANT");
+    v = (env && env[0] == '3') ? 3 : 2;
+  }
+  return v == 3 && hidden % 64 == 0 && n_experts <= 64;  // EP = 128 spills in v3 (round 2)
+}
+
+static int pair_chunks(int hidden, int n_experts) {
+  return use_v3(hidden, n_experts) ? (hidden + 191) / 192 : hidden / HC;
+}
+
 // Chunk groups per tile: only when the tiles leave CTA pairs idle (fewer tiles
 // than pairs); then the fewest pair-rounds of chunks, ties to fewer groups.
 // Large N never splits (the partial-logit traffic and the x re-streaming would
 // cost more than the last-wave imbalance they remove).
-static int choose_split(int64_t n_tokens, int hidden, int n_pairs) {
-  const int nchunks = hidden / HC;
+static int choose_split(int64_t n_tokens, int nchunks, int n_pairs) {
   const int64_t tiles = (n_tokens + 2 * BM - 1) / (2 * BM);
   if (tiles >= n_pairs) return 1;
   const int64_t cost1 = ((tiles + n_pairs - 1) / n_pairs) * nchunks;
   int best = 1;
   int64_t best_cost = cost1;
-  for (int g = 2; g <= nchunks && g <= 16; g *= 2) {
+  for (int g = 2; g <= nchunks && g <= 16; ++g) {
     if (nchunks % g) continue;
     const int64_t cost = ((tiles * g + n_pairs - 1) / n_pairs) * (nchunks / g);
     if (cost < best_cost) { best = g; best_cost = cost; }
@@ -635,14 +652,18 @@ extern "C" int moep_k1_prof(unsigned long long* host, int reset) {
 
 extern "C" int64_t moep_predict_split_floats(int64_t n_tokens, int32_t hidden, int32_t n_experts) {
   using namespace moep::k1v2;
-  if (n_tokens <= 0 || hidden <= 0 || hidden % HC != 0 || n_experts <= 0 || n_experts > 128) return 0;
-  const int g = choose_split(n_tokens, hidden, moep_num_sms() / 2);
+  if (n_tokens <= 0 || hidden <= 0 || n_experts <= 0 || n_experts > 128) return 0;
+  if (hidden % HC != 0 && !use_v3(hidden, n_experts)) return 0;
+  const int g = choose_split(n_tokens, pair_chunks(hidden, n_experts), moep_num_sms() / 2);
   if (g == 1) return 0;
   int EP = 16;
   while (EP < n_experts) EP *= 2;
   const int64_t zpad = ((n_tokens + 2 * BM - 1) / (2 * BM)) * 2 * BM;
   return static_cast<int64_t>(g) * zpad * (EP + 1);
 }
+
+extern "C" int moep_predict_bf16_pair3(const moep_predict_args* a, int split, float* zpart, int64_t zpad,
+                                       void* stream);
 
 namespace {
 template <int EP, int ARCH>
@@ -677,12 +698,17 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
   p.split = 1; p.zpart = nullptr; p.zpad = 0;
   const int64_t need = moep_predict_split_floats(a->n_tokens, a->hidden, a->n_experts);
   if (need > 0 && a->split_scratch && a->split_scratch_floats >= need) {
-    p.split = choose_split(a->n_tokens, a->hidden, grid / 2);
+    p.split = choose_split(a->n_tokens, pair_chunks(a->hidden, a->n_experts), grid / 2);
     p.zpart = a->split_scratch;
     p.zpad = ((a->n_tokens + 2 * BM - 1) / (2 * BM)) * 2 * BM;
   }
-  kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);
-  if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
+  if (use_v3(a->hidden, a->n_experts)) {
+    const int rc = moep_predict_bf16_pair3(a, p.split, p.zpart, p.zpad, st);
+    if (rc != MOEP_OK) return rc;
+  } else {
+    kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);
+    if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
+  }
   if (p.split > 1) {
     split_finish_kernel<EP><<<moep_num_sms(), 256, 0, st>>>(p);
     if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
@@ -693,7 +719,8 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
 
 // Pair kernel entry (validation shared with moep_predict_bf16, which dispatches here).
 extern "C" int moep_predict_bf16_pair(const moep_predict_args* a, void* stream) {
-  if (a->hidden % 256 != 0 || a->n_experts > 128) return MOEP_EUNSUPPORTED;
+  if (a->n_experts > 128) return MOEP_EUNSUPPORTED;
+  if (a->hidden % 256 != 0 && !moep::k1v2::use_v3(a->hidden, a->n_experts)) return MOEP_EUNSUPPORTED;
   int EP = 16;
   while (EP < a->n_experts) EP *= 2;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

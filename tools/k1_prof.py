@@ -42,7 +42,9 @@ if __name__ == "__main__":
     import bench
     from paper_2511_10676_b200 import _lib
     L = _lib.lib()
-    L.moep_k1_prof.argtypes = [C.c_void_p, C.c_int]
+    V3 = os.environ.get("MOEP_K1_VARIANT", "3") != "2"
+    prof = L.moep_k1v3_prof if V3 else L.moep_k1_prof
+    prof.argtypes = [C.c_void_p, C.c_int]
     layers = bench.make_layers(torch.device("cuda"), 1, bench.TOKENS, 0)
     _, dp, x, t = layers[0]
     part = torch.empty((148, 136), dtype=torch.int32, device="cuda")
@@ -50,12 +52,12 @@ if __name__ == "__main__":
     for _ in range(3):
         run()
     torch.cuda.synchronize()
-    L.moep_k1_prof(None, 1)
+    prof(None, 1)
     run()
     torch.cuda.synchronize()
     import numpy as np
     buf = np.zeros((160, 16), dtype=np.uint64)
-    L.moep_k1_prof(buf.ctypes.data, 0)
+    prof(buf.ctypes.data, 0)
     names = {0: "TMA x/W1: wait empty (ring full)", 1: "TMA W2: wait w2_empty", 2: "MMA: wait z_empty",
              3: "MMA: wait w2_full", 4: "MMA: wait a2_full (block)", 5: "MMA: wait acc_empty",
              6: "MMA: wait full (operands)", 7: "EPI WG0: wait acc_full", 8: "EPI WG0: wait a2_emptyB",
@@ -66,4 +68,4 @@ if __name__ == "__main__":
     tot = lead[:, 15].astype(float).mean()
     for s_, n in names.items():
         v = lead[:, s_].astype(float).mean()
-        print(f"{n:44s} {v / tot * 100:6.2f} %  ({v:.0f} cycles, {v / 448:.0f} per chunk)")
+        print(f"{n:44s} {v / tot * 100:6.2f} %  ({v:.0f} cycles, {v / 448:.0f} per chunk)")  # v3: 11 chunks / tile
