@@ -42,7 +42,7 @@ if __name__ == "__main__":
     import bench
     from paper_2511_10676_b200 import _lib
     L = _lib.lib()
-    V3 = os.environ.get("MOEP_K1_VARIANT", "3") != "2"
+    V3 = os.environ.get("MOEP_K1_VARIANT", "2") == "3"
     prof = L.moep_k1v3_prof if V3 else L.moep_k1_prof
     prof.argtypes = [C.c_void_p, C.c_int]
     layers = bench.make_layers(torch.device("cuda"), 1, bench.TOKENS, 0)
