@@ -131,12 +131,27 @@ order_kernel(const T* __restrict__ z, int64_t n, int E, int* __restrict__ order)
   }
 }
 
-__global__ void reduce_kernel(const int* __restrict__ partials, int n_blocks, int n_counters,
-                              long long* __restrict__ out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_counters; c += gridDim.x * blockDim.x) {
-    long long s = 0;
-    for (int b = 0; b < n_blocks; ++b) s += partials[static_cast<int64_t>(b) * n_counters + c];
-    out[c] = s;
+// Counter reduction. int64 sums are exact, so the summation order does not
+// change the result. Block = 32 counters x 32 warps: lanes read
+// 32 consecutive counters of one partial row (coalesced), the 32 warps of the
+// block split the partial rows, then a shared-memory tree.
+__global__ void __launch_bounds__(1024) reduce_kernel(const int* __restrict__ partials, int n_blocks,
+                                                      int n_counters, long long* __restrict__ out) {
+  __shared__ long long red[32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  long long s = 0;
+  if (c < n_counters) {
+#pragma unroll 4
+    for (int b = w; b < n_blocks; b += 32) s += partials[static_cast<int64_t>(b) * n_counters + c];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0) {
+    long long t = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t += red[i][lane];
+    if (c < n_counters) out[c] = t;
   }
 }
 
@@ -290,7 +305,7 @@ int moep_counters_reduce(const int32_t* partials, int32_t n_blocks, int32_t n_co
                          void* stream) {
   if (n_blocks <= 0 || n_counters <= 0) return MOEP_ESHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  moep::k7::reduce_kernel<<<(n_counters + 255) / 256, 256, 0, st>>>(
+  moep::k7::reduce_kernel<<<(n_counters + 31) / 32, 1024, 0, st>>>(
       partials, n_blocks, n_counters, reinterpret_cast<long long*>(out));
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }

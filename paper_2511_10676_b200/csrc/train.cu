@@ -76,10 +76,11 @@ __device__ __forceinline__ double sigm(double u) {
   return eu / (1.0 + eu);
 }
 
+// Generic fallback (E > 512): one warp per token.
 // partials per CTA: [0] loss (bce/mse/focal part), [1] hinge total (unnormalised), [2] n_pairs
 template <typename T>
 __global__ void __launch_bounds__(NT)
-loss_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restrict__ rank_of,
+loss_rowwarp_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restrict__ rank_of,
             const uint8_t* __restrict__ mask, int64_t n, int E, LossParams p, T* __restrict__ dz,
             T* __restrict__ dz_hinge, double* __restrict__ partials) {
   __shared__ double red[NT / 32][3];
@@ -183,16 +184,174 @@ loss_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restr
   }
 }
 
+// partials per CTA: [0] loss (bce/mse/focal part), [1] hinge total (unnormalised), [2] n_pairs.
+// LPR lanes per token (a power of two <= 32, so a warp holds 32/LPR tokens),
+// EPL experts per lane (expert e = lane_in_row + i*LPR). The token's logits,
+// scores and ranks stay in registers; the pairwise hinge walks the row by
+// width-LPR shuffles instead of re-reading global memory.
+template <typename T, int LPR, int EPL>
+__global__ void __launch_bounds__(NT)
+loss_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restrict__ rank_of,
+            const uint8_t* __restrict__ mask, int64_t n, int E, LossParams p, T* __restrict__ dz,
+            T* __restrict__ dz_hinge, double* __restrict__ partials) {
+  constexpr int RPW = 32 / LPR;
+  __shared__ double red[NT / 32][3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / LPR, li = lane % LPR;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  double l_main = 0.0, l_hinge = 0.0, n_pairs = 0.0;
+  for (int64_t base = gw * RPW; base < n; base += nw * RPW) {  // warp-uniform
+    const int64_t row = base + sub;
+    double zv[EPL], sv[EPL];
+    int rk[EPL];
+    bool pos[EPL], ev[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      const int e = li + i * LPR;
+      ev[i] = row < n && e < E;
+      const int64_t o = row * E + e;
+      zv[i] = ev[i] ? static_cast<double>(z[o]) : 0.0;
+      sv[i] = ev[i] ? static_cast<double>(s[o]) : 0.0;
+      rk[i] = ev[i] ? rank_of[o] : 0x7fffffff;
+      pos[i] = ev[i] && mask[o] != 0;
+    }
+    if (p.family == 0) {
+      // MSE on softmax probabilities (losses.py:99-110, chain rule :250-255)
+      double mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i)
+        if (ev[i]) mx = fmax(mx, zv[i]);
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      double ex[EPL], se = 0.0;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        ex[i] = ev[i] ? exp(zv[i] - mx) : 0.0;
+        se += ex[i];
+      }
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+      double inner = 0.0;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        if (!ev[i]) continue;
+        ex[i] /= se;  // probability
+        const double diff = sv[i] - ex[i];
+        l_main += diff * diff * p.inv_n;
+        inner += (-2.0 * diff * p.inv_n) * ex[i];
+      }
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) inner += __shfl_xor_sync(0xffffffffu, inner, o);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        if (!ev[i]) continue;
+        const double dp = -2.0 * (sv[i] - ex[i]) * p.inv_n;
+        dz[row * E + li + i * LPR] = static_cast<T>(ex[i] * (dp - inner));
+      }
+      continue;
+    }
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      if (!ev[i]) continue;
+      const double zi = zv[i];
+      double g = 0.0;
+      if (p.family == 2) {
+        // focal (losses.py:156-179)
+        const double log_pt = pos[i] ? -softplus(-zi) : -softplus(zi);
+        const double pt = exp(log_pt);
+        const double at = pos[i] ? p.alpha : 1.0 - p.alpha;
+        const double om = 1.0 - pt;
+        const double focus = pow(om, p.gamma);
+        l_main += -at * focus * log_pt * p.inv_ne;
+        const double sgn = pos[i] ? 1.0 : -1.0;
+        g = at * sgn * (p.gamma * pt * focus * log_pt - pow(om, p.gamma + 1.0)) * p.inv_ne;
+      } else if (p.family != 4) {
+        // tier weights (losses.py:113-121); three tiers only for the ranking family
+        const int r = rk[i];
+        double w = p.rest_w;
+        if (p.family == 3 && r > p.top_cut && r <= p.mid_cut) w = p.mid_w;
+        if (r <= p.top_cut) w = p.top_w;
+        const double lt = pos[i] ? -softplus(-zi) : -softplus(zi);
+        l_main += -w * lt * p.inv_ne;
+        g = w * (sigm(zi) - (pos[i] ? 1.0 : 0.0)) * p.inv_ne;
+      }
+      dz[row * E + li + i * LPR] = static_cast<T>(g);  // family 4 (hinge only): 0
+    }
+    if (p.family >= 3) {
+      // pairwise hinge over the true top-T (losses.py:182-217), unnormalised here;
+      // each strict pair is counted by its higher-scored member
+      double gh[EPL];
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) gh[i] = 0.0;
+#pragma unroll
+      for (int jb = 0; jb < EPL; ++jb) {
+        for (int jl = 0; jl < LPR; ++jl) {
+          const int j = jb * LPR + jl;
+          if (j >= E) break;
+          const double sj = __shfl_sync(0xffffffffu, sv[jb], jl, LPR);
+          const double zj = __shfl_sync(0xffffffffu, zv[jb], jl, LPR);
+          const int rj = __shfl_sync(0xffffffffu, rk[jb], jl, LPR);
+          const bool jtop = rj <= p.top_cut;  // (no divergent exit before the next shuffles)
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) {
+            if (!jtop || !ev[i] || rk[i] > p.top_cut || li + i * LPR == j) continue;
+            if (sv[i] > sj) {  // e outranks j in truth: pair (e, j)
+              n_pairs += 1.0;
+              const double gap = p.margin - (zv[i] - zj);
+              if (gap > 0) { l_hinge += gap; gh[i] -= 1.0; }
+            } else if (sj > sv[i]) {  // pair (j, e)
+              const double gap = p.margin - (zj - zv[i]);
+              if (gap > 0) gh[i] += 1.0;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < EPL; ++i)
+        if (ev[i]) dz_hinge[row * E + li + i * LPR] = static_cast<T>(gh[i]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l_main += __shfl_xor_sync(0xffffffffu, l_main, o);
+    l_hinge += __shfl_xor_sync(0xffffffffu, l_hinge, o);
+    n_pairs += __shfl_xor_sync(0xffffffffu, n_pairs, o);
+  }
+  if (lane == 0) { red[warp][0] = l_main; red[warp][1] = l_hinge; red[warp][2] = n_pairs; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
+    partials[blockIdx.x * 3 + threadIdx.x] = v;
+  }
+}
+
 // sums partials in a fixed order; ranking: dz += lam/n_pairs * dz_hinge
 template <typename T>
 __global__ void finalize_kernel(const double* __restrict__ partials, int nblk, int64_t n, int E, int family,
                                 double lam, int normalize, T* __restrict__ dz,
                                 const T* __restrict__ dz_hinge, double* __restrict__ out_loss) {
+  // fixed-order tree over the partial rows (the same order in every block, so
+  // the total is deterministic): thread t sums rows t, t+256, ..., then a
+  // shared-memory halving tree (blockDim.x == 256)
   __shared__ double tot[3];
-  if (threadIdx.x < 3) {
-    double v = 0.0;
-    for (int b = 0; b < nblk; ++b) v += partials[b * 3 + threadIdx.x];
-    tot[threadIdx.x] = v;
+  __shared__ double acc[3][256];
+  {
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += 256) {
+      v0 += partials[b * 3 + 0];
+      v1 += partials[b * 3 + 1];
+      v2 += partials[b * 3 + 2];
+    }
+    acc[0][threadIdx.x] = v0; acc[1][threadIdx.x] = v1; acc[2][threadIdx.x] = v2;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+      if (threadIdx.x < h)
+        for (int c = 0; c < 3; ++c) acc[c][threadIdx.x] += acc[c][threadIdx.x + h];
+      __syncthreads();
+    }
+    if (threadIdx.x < 3) tot[threadIdx.x] = acc[threadIdx.x][0];
   }
   __syncthreads();
   double scale = 0.0;
@@ -523,6 +682,30 @@ __global__ void optim_kernel(T* __restrict__ p, const T* __restrict__ g, T* __re
 
 using namespace moep::tr;
 
+template <typename T>
+static int launch_loss(const moep_loss_args* a, const LossParams& p, cudaStream_t st) {
+  const T* z = static_cast<const T*>(a->logits);
+  const T* sc = static_cast<const T*>(a->scores);
+  T* dz = static_cast<T*>(a->dz);
+  T* dzh = static_cast<T*>(a->dz_hinge);
+  const int E = a->n_experts;
+#define MOEP_K4(LPR, EPL)                                                                                   \
+  loss_kernel<T, LPR, EPL><<<a->n_blocks, NT, 0, st>>>(z, sc, a->rank_of, a->topk_mask, a->n, E, p, dz, dzh, \
+                                                       a->partials)
+  if (E <= 8) MOEP_K4(8, 1);
+  else if (E <= 16) MOEP_K4(16, 1);
+  else if (E <= 32) MOEP_K4(32, 1);
+  else if (E <= 64) MOEP_K4(32, 2);
+  else if (E <= 128) MOEP_K4(32, 4);
+  else if (E <= 256) MOEP_K4(32, 8);
+  else if (E <= 512) MOEP_K4(32, 16);
+  else
+    loss_rowwarp_kernel<T><<<a->n_blocks, NT, 0, st>>>(z, sc, a->rank_of, a->topk_mask, a->n, E, p, dz, dzh,
+                                                       a->partials);
+#undef MOEP_K4
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
 extern "C" {
 
 int moep_labels(const void* scores, int32_t dtype, int64_t n, int32_t E, int32_t k, int32_t* rank_of,
@@ -557,16 +740,10 @@ int moep_loss(const moep_loss_args* a, void* stream) {
   p.inv_ne = 1.0 / (static_cast<double>(a->n_global) * a->n_experts);
   p.inv_n = 1.0 / static_cast<double>(a->n_global);
   if (a->dtype == MOEP_F64)
-    loss_kernel<double><<<a->n_blocks, NT, 0, st>>>(
-        static_cast<const double*>(a->logits), static_cast<const double*>(a->scores), a->rank_of, a->topk_mask,
-        a->n, a->n_experts, p, static_cast<double*>(a->dz), static_cast<double*>(a->dz_hinge), a->partials);
-  else if (a->dtype == MOEP_F32)
-    loss_kernel<float><<<a->n_blocks, NT, 0, st>>>(
-        static_cast<const float*>(a->logits), static_cast<const float*>(a->scores), a->rank_of, a->topk_mask,
-        a->n, a->n_experts, p, static_cast<float*>(a->dz), static_cast<float*>(a->dz_hinge), a->partials);
-  else
-    return MOEP_EARG;
-  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+    return launch_loss<double>(a, p, st);
+  if (a->dtype == MOEP_F32)
+    return launch_loss<float>(a, p, st);
+  return MOEP_EARG;
 }
 
 int moep_loss_finalize(const double* partials, int32_t n_blocks, int64_t n, int32_t E, int32_t family,
