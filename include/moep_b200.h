@@ -294,6 +294,24 @@ int moep_gather_experts(const void* host_mapped_store, int64_t expert_bytes, con
                         const int32_t* need_slot, const int32_t* need_count, void* cache, int32_t n_ctas,
                         void* stream);
 
+/* ------------------------------------------------------------------ K11 --
+ * Synthetic teacher (synthgen.py:162-189). Sample first_index+i draws from
+ * numpy.random.Generator(Philox(key=(seed << 64) + first_index + i))
+ * (synthgen.py:44-47): d standard normals into row i of x64 (fp64) and/or x32
+ * (fp32 cast), then, with with_noise, d more into noise64 (synthgen.py:170-174).
+ * Normals follow numpy's ziggurat (random_standard_normal). */
+int moep_teacher_normals(uint64_t seed, int64_t first_index, int64_t n, int32_t d, int32_t with_noise,
+                         double* x64, float* x32, double* noise64, void* stream);
+/* core.layer_norm (core.py:57-68) row-wise over [n, d] fp64 with numpy's
+ * reduction order (0 + pairwise_sum) and single roundings: bit-identical to
+ * numpy. out may alias x. */
+int moep_layer_norm_np(const double* x, int64_t n, int32_t d, double eps, double* out, void* stream);
+/* gate softmax (core.py:19-24) of fp64 logits [n, E] in numpy order, float32
+ * scores [n, E] and ascending top-k ids [n, k] of the float32 scores
+ * (make_dataset, synthgen.py:148-159; core.py:42-48). E <= 256. */
+int moep_teacher_finish(const double* logits, int64_t n, int32_t n_experts, int32_t k, float* scores,
+                        int32_t* topk, void* stream);
+
 /* ---------------------------------------------------------------- misc -- */
 int moep_num_sms(void);
 const char* moep_version(void);

@@ -37,7 +37,7 @@ def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.inc")) + [
         os.path.join(HERE, "..", "include", "moep_b200.h")]
     return all(os.path.getmtime(p) <= t for p in deps if os.path.exists(p))
 

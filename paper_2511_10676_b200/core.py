@@ -3,8 +3,8 @@
 `top_k`, `top_k_batch` and `rank_order` keep the reference contract — stable
 descending order, ties to the lower index, `top_k*` returned ascending
 (core.py:27-54) — and run on the GPU through K7 (`moep_topk_logits`).
-`softmax` and `layer_norm` are small fp64 helpers evaluated with torch on the
-device. numpy in -> numpy out; CUDA tensors in -> CUDA tensors out.
+`softmax` is a small fp64 torch helper on the device; `layer_norm` runs the
+K11b kernel with numpy's summation order (bit-identical to the reference). numpy in -> numpy out; CUDA tensors in -> CUDA tensors out.
 """
 
 from __future__ import annotations
@@ -66,13 +66,22 @@ def rank_order(scores):
 
 
 def layer_norm(x, eps: float = LAYER_NORM_EPS):
-    """Non-affine layer norm, population variance (core.py:57-68)."""
+    """Non-affine layer norm, population variance (core.py:57-68).
+
+    K11b `moep_layer_norm_np`: numpy's reduction order (0 + pairwise_sum) and
+    single roundings, so the result is bit-identical to the reference's."""
+    from ._lib import check, lib, ptr
     t, is_t = _to_device(x)
     if t.shape[-1] < 2:
         raise ValueError("layer_norm needs at least 2 elements")
-    mu = t.mean(dim=-1, keepdim=True)
-    var = ((t - mu) ** 2).mean(dim=-1, keepdim=True)
-    out = (t - mu) / torch.sqrt(var + eps)
+    shape = t.shape
+    flat = t.reshape(-1, shape[-1]).contiguous()
+    out = torch.empty_like(flat)
+    if flat.shape[0] > 0:
+        check(lib().moep_layer_norm_np(ptr(flat), flat.shape[0], flat.shape[1], float(eps), ptr(out),
+                                       torch.cuda.current_stream(flat.device).cuda_stream),
+              "moep_layer_norm_np")
+    out = out.reshape(shape)
     return out if is_t else out.cpu().numpy()
 
 

@@ -3,7 +3,7 @@ build container. The reference lives at /root/reference and does not exist on
 the GPU box, so its outputs are frozen here as small .npz files that
 tests/test_oracle_golden.py (CPU) and the -m gpu parity tests consume.
 
-Run:  PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+Run:  PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [synthgen]
 """
 
 from __future__ import annotations
@@ -203,13 +203,57 @@ def trace_cases():
     return out
 
 
+SYNTH_CASES = [
+    # name, d, E, k, n, seed, transform, post_norm, noise_sigma, nonlinear_hidden
+    ("dsv2l_identity", 2048, 64, 6, 24, 3, "identity", True, 0.0, 64),
+    ("nonlinear_noise", 256, 16, 2, 40, 5, "nonlinear", True, 0.1, 32),
+    ("linear_raw", 128, 128, 8, 24, 7, "linear", False, 0.0, 64),
+    ("identity_noise_raw", 96, 8, 3, 30, 11, "identity", False, 0.25, 64),
+]
+
+
+def synthgen_cases():
+    """synthgen.generate_dataset (synthgen.py:162-189) of the real reference
+    for four teachers (transforms, noise, post_norm on/off, odd d)."""
+    from moepredict import synthgen
+    out = {}
+    for name, d, e, k, n, seed, transform, post_norm, sigma, nh in SYNTH_CASES:
+        gate = np.random.default_rng(seed + 100).standard_normal((e, d)) / np.sqrt(d)
+        router = core.RouterSpec(d, e, k, gate)
+        teacher = synthgen.TeacherSpec(router, transform=transform, post_norm=post_norm, noise_sigma=sigma,
+                                       nonlinear_hidden=nh, seed=seed)
+        data = synthgen.generate_dataset(teacher, n)
+        out[name + "_gate"] = gate
+        out[name + "_x"] = data.activations
+        out[name + "_scores"] = data.true_scores
+        out[name + "_topk"] = data.true_topk
+        # raw fp64 normals of the first 2 samples (activation then noise row)
+        raw = []
+        for i in range(2):
+            g = synthgen._rng(seed, i)
+            raw.append(g.standard_normal(2 * d))
+        out[name + "_raw"] = np.stack(raw)
+    # layer_norm of wide-magnitude rows (numpy reduction order)
+    rng = np.random.default_rng(9)
+    for d in (2048, 1000, 129, 7):
+        x = rng.standard_normal((6, d)) * np.exp(2 * rng.standard_normal((6, d))) + 3.0
+        out[f"ln_{d}_x"] = x
+        out[f"ln_{d}_y"] = core.layer_norm(x)
+    return out
+
+
 def main():
+    if sys.argv[1:] == ["synthgen"]:
+        np.savez_compressed(os.path.join(HERE, "synthgen.npz"), **synthgen_cases())
+        print("synthgen.npz", os.path.getsize(os.path.join(HERE, "synthgen.npz")))
+        return
     np.savez_compressed(os.path.join(HERE, "topk.npz"), **topk_cases())
     np.savez_compressed(os.path.join(HERE, "predictor.npz"), **predictor_cases())
     np.savez_compressed(os.path.join(HERE, "losses.npz"), **loss_cases())
     np.savez_compressed(os.path.join(HERE, "metrics.npz"), **metric_cases())
     np.savez_compressed(os.path.join(HERE, "optim.npz"), **adam_cases())
     np.savez_compressed(os.path.join(HERE, "trace.npz"), **trace_cases())
+    np.savez_compressed(os.path.join(HERE, "synthgen.npz"), **synthgen_cases())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
