@@ -7,7 +7,7 @@
 //                          from numpy by tools/gen_ziggurat_tables.py), the
 //                          activation row then the noise row of each sample
 //                          (synthgen.py:170-174). One thread per sample; rows
-//                          staged 32 values at a time in shared memory so the
+//                          staged 16 values at a time in shared memory so the
 //                          HBM writes are coalesced.
 //   moep_layer_norm_np     core.layer_norm (core.py:57-68) with numpy's exact
 //                          reduction order: add.reduce = 0 + pairwise_sum
@@ -41,15 +41,21 @@ constexpr uint64_t kM0 = 0xD2E7470EE14C6C93ull, kM1 = 0xCA5A826395121157ull;
 constexpr uint64_t kW0 = 0x9E3779B97F4A7C15ull, kW1 = 0xBB67AE8584CAA73Bull;
 constexpr double kZigR = 3.6541528853610088, kZigInvR = 0.27366123732975828;
 
-// numpy.random.Philox(key=...) stream: 4-word buffer refilled by Philox4x64-10
-// of the counter incremented first (counter starts at 0).
+// numpy.random.Philox(key=...) stream: each refill is Philox4x64-10 of the
+// counter incremented first (counter starts at 0), 4 words in stream order.
+//
+// Words sit in a per-thread 8-entry FIFO in shared memory. The caller refills
+// in lockstep once per 4 normals (all lanes together: no divergent Philox
+// rounds), and a lane whose FIFO runs dry after a slow-path draw refills on
+// its own (`next64`). Every normal consumes >= 1 word, so at each lockstep
+// point at most 3 words remain and the FIFO never holds more than 7.
 struct PhiloxStream {
   uint64_t k0, k1, c0, c1;
-  uint64_t b0, b1, b2, b3;
-  int pos;
+  unsigned head, tail;   // words consumed / produced
+  uint64_t* fifo;        // 8 words (stride-padded row of a shared array)
 
-  __device__ void init(uint64_t key_lo, uint64_t key_hi) {
-    k0 = key_lo; k1 = key_hi; c0 = 0; c1 = 0; pos = 4;
+  __device__ void init(uint64_t key_lo, uint64_t key_hi, uint64_t* f) {
+    k0 = key_lo; k1 = key_hi; c0 = 0; c1 = 0; head = 0; tail = 0; fifo = f;
   }
   __device__ void refill() {
     if (++c0 == 0) ++c1;
@@ -62,13 +68,12 @@ struct PhiloxStream {
       x0 = n0; x1 = lo1; x2 = n2; x3 = lo0;
       y0 += kW0; y1 += kW1;
     }
-    b0 = x0; b1 = x1; b2 = x2; b3 = x3;
+    fifo[tail & 7] = x0; fifo[(tail + 1) & 7] = x1; fifo[(tail + 2) & 7] = x2; fifo[(tail + 3) & 7] = x3;
+    tail += 4;
   }
   __device__ uint64_t next64() {
-    if (pos >= 4) { refill(); pos = 0; }
-    const uint64_t v = pos == 0 ? b0 : pos == 1 ? b1 : pos == 2 ? b2 : b3;
-    ++pos;
-    return v;
+    if (head == tail) refill();
+    return fifo[(head++) & 7];
   }
   __device__ double next_double() {
     return static_cast<double>(next64() >> 11) * (1.0 / 9007199254740992.0);
@@ -78,16 +83,17 @@ struct PhiloxStream {
 // numpy random_standard_normal (distributions.c): one 64-bit word = 8 layer
 // bits, 1 sign bit, 52 mantissa bits; tail (layer 0) by -log1p(-U) pairs;
 // wedge test against exp(-x^2/2).
-__device__ double standard_normal(PhiloxStream& s) {
+__device__ double standard_normal(PhiloxStream& s, const unsigned long long* __restrict__ ki,
+                                  const double* __restrict__ wi) {
   for (;;) {
     uint64_t r = s.next64();
     const int idx = static_cast<int>(r & 0xff);
     r >>= 8;
     const bool neg = r & 1;
     const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-    double x = __dmul_rn(static_cast<double>(rabs), kZigWi[idx]);
+    double x = __dmul_rn(static_cast<double>(rabs), wi[idx]);
     if (neg) x = -x;
-    if (rabs < kZigKi[idx]) return x;
+    if (rabs < ki[idx]) return x;
     if (idx == 0) {
       for (;;) {
         const double xx = __dmul_rn(-kZigInvR, log1p(-s.next_double()));
@@ -104,31 +110,43 @@ __device__ double standard_normal(PhiloxStream& s) {
 }
 
 constexpr int NB = 128;  // samples per block
+constexpr int SEG = 16;  // values per sample staged between coalesced writes
 
-__global__ void __launch_bounds__(NB)
+__global__ void __launch_bounds__(NB, 8)
 normals_kernel(uint64_t seed, int64_t first, int64_t n, int d, int with_noise, double* __restrict__ x64,
                float* __restrict__ x32, double* __restrict__ nz64) {
-  __shared__ double stage[NB][33];
+  __shared__ double stage[NB][SEG + 1];
+  __shared__ uint64_t s_fifo[NB][9];
+  __shared__ unsigned long long s_ki[256];
+  __shared__ double s_wi[256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 256; i += NB) { s_ki[i] = kZigKi[i]; s_wi[i] = kZigWi[i]; }
+  __syncthreads();
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * NB;
   const bool valid = i0 + tid < n;
   PhiloxStream s;
   // key = (seed << 64) + index (synthgen.py:46), index < 2^63
-  s.init(static_cast<uint64_t>(first + i0 + tid), seed);
+  s.init(static_cast<uint64_t>(first + i0 + tid), seed, s_fifo[tid]);
+  unsigned g = 0;  // normals drawn so far (both rows): lockstep refill every 4
   for (int pass = 0; pass < (with_noise ? 2 : 1); ++pass) {
     double* out = pass ? nz64 : x64;
-    for (int j0 = 0; j0 < d; j0 += 32) {
-      const int cnt = min(32, d - j0);
-      if (valid)
-        for (int t = 0; t < cnt; ++t) stage[tid][t] = standard_normal(s);
+    for (int j0 = 0; j0 < d; j0 += SEG) {
+      const int cnt = min(SEG, d - j0);
+      if (valid) {
+        for (int t = 0; t < cnt; ++t, ++g) {
+          if ((g & 3) == 0 && s.tail - s.head < 4) s.refill();
+          stage[tid][t] = standard_normal(s, s_ki, s_wi);
+        }
+      }
       __syncthreads();
-      // warp w writes the 32-value segments of samples w*32 .. w*32+31
-      for (int rr = 0; rr < 32; ++rr) {
-        const int row = warp * 32 + rr;
+      // warp w writes the SEG-value segments of samples w*32 .. w*32+31,
+      // 32 / SEG samples per store instruction
+      for (int rr = 0; rr < 32; rr += 32 / SEG) {
+        const int row = warp * 32 + rr + lane / SEG, col = lane % SEG;
         const int64_t gi = i0 + row;
-        if (gi < n && lane < cnt) {
-          const double v = stage[row][lane];
-          const int64_t o = gi * d + j0 + lane;
+        if (gi < n && col < cnt) {
+          const double v = stage[row][col];
+          const int64_t o = gi * d + j0 + col;
           if (out) out[o] = v;
           if (pass == 0 && x32) x32[o] = __double2float_rn(v);
         }
@@ -244,7 +262,19 @@ __global__ void layer_norm_np_kernel(const double* __restrict__ x, int64_t n, in
   const double dd = static_cast<double>(d);
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * nwarps + warp; r < n; r += static_cast<int64_t>(gridDim.x) * nwarps) {
     const double* xr = x + r * d;
-    for (int i = lane; i < d; i += 32) row[pad(i)] = xr[i];
+    if ((d & 1) == 0 && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
+      // 16-byte streaming loads, 16 in flight per lane
+      const double2* x2 = reinterpret_cast<const double2*>(xr);
+#pragma unroll 16
+      for (int i = lane; i < d / 2; i += 32) {
+        const double2 v = __ldcs(x2 + i);
+        row[pad(2 * i)] = v.x;
+        row[pad(2 * i + 1)] = v.y;
+      }
+    } else {
+#pragma unroll 8
+      for (int i = lane; i < d; i += 32) row[pad(i)] = __ldcs(xr + i);
+    }
     __syncwarp();
     const double mean = __ddiv_rn(warp_pairwise<0>(row, plan, 0.0, leafsum, lane), dd);
     const double var = __ddiv_rn(warp_pairwise<1>(row, plan, mean, leafsum, lane), dd);
@@ -362,8 +392,8 @@ int moep_layer_norm_np(const double* x, int64_t n, int32_t d, double eps, double
   if (n <= 0 || d < 2) return MOEP_ESHAPE;
   if (leaf_cap(d) > kMaxLeaves) return MOEP_EUNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int nwarps = 8;
-  while (nwarps > 1 && plan_smem(nwarps, d) > 200 * 1024) nwarps >>= 1;
+  int nwarps = 16;
+  while (nwarps > 1 && plan_smem(nwarps, d) > 220 * 1024) --nwarps;
   const size_t sm = plan_smem(nwarps, d);
   if (sm > 227 * 1024) return MOEP_EUNSUPPORTED;
   if (cudaFuncSetAttribute(layer_norm_np_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

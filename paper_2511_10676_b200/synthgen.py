@@ -151,7 +151,7 @@ class _Teacher:
               "moep_teacher_finish")
 
 
-def generate_dataset_device(teacher: TeacherSpec, n: int, device="cuda", chunk_rows: int = 65536,
+def generate_dataset_device(teacher: TeacherSpec, n: int, device="cuda", chunk_rows: int = 262144,
                             first_index: int = 0) -> DeviceTrace:
     """generate_dataset (synthgen.py:162-189) into HBM: activations fp32 [n, d],
     scores fp32 [n, E], top-k int32 [n, k] ascending."""

@@ -83,6 +83,26 @@ def main():
         kbest = min(kbest, s0.elapsed_time(s1))
     normals = m * d * (2 if a.noise > 0 else 1)
     bytes_w = m * d * 12 + (m * d * 8 if a.noise > 0 else 0)
+    # stage breakdown of one 262144-sample chunk (the default chunk of generate_dataset_device)
+    c = min(a.n, 262144)
+    tt = sg._Teacher(t, torch.device("cuda"))
+    acts = torch.empty((c, d), dtype=torch.float32, device="cuda")
+    sc = torch.empty((c, e), dtype=torch.float32, device="cuda")
+    tk = torch.empty((c, k), dtype=torch.int32, device="cuda")
+    x64c = torch.empty((c, d), dtype=torch.float64, device="cuda")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    for rep in range(2):
+        ev[0].record()
+        check(lib().moep_teacher_normals(seed, 0, c, d, 0, ptr(x64c), ptr(acts), None, st), "normals")
+        ev[1].record()
+        check(lib().moep_layer_norm_np(ptr(x64c), c, d, 1e-5, ptr(x64c), st), "ln")
+        ev[2].record()
+        logits = torch.mm(x64c, tt.gate_t)
+        ev[3].record()
+        check(lib().moep_teacher_finish(ptr(logits), c, e, k, ptr(sc), ptr(tk), st), "finish")
+        ev[4].record()
+        torch.cuda.synchronize()
+    stages = {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(["normals", "layer_norm", "gate_gemm", "finish"])}
     cpu = cpu_reference(gate, a.cpu_n, d, a.noise, seed)
     res = {"workload": "DSV2L-shaped teacher (d=2048, E=64, top-6, identity + layer_norm"
                        + (f", noise {a.noise}" if a.noise > 0 else "") + ")",
@@ -91,7 +111,8 @@ def main():
                               "write_gbs": bytes_w / (kbest / 1e3) / 1e9},
            "cpu_reference": {"samples_per_s": cpu, "sample": f"{a.cpu_n} samples, numpy per-sample Philox loop "
                              "(synthgen.py:170-174) + layer_norm + gate softmax + top-k", "cores": os.cpu_count()},
-           "speedup_vs_cpu": a.n / (best / 1e3) / cpu}
+           "speedup_vs_cpu": a.n / (best / 1e3) / cpu,
+           "stages_ms_per_chunk": stages, "chunk": c}
     print(json.dumps(res))
     if a.out:
         with open(a.out, "w") as f:
