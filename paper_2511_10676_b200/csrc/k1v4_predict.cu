@@ -1,24 +1,19 @@
-// k1v2_predict.cu — K1 v2: fused expert predictor on a CTA pair (cta_group::2).
+// k1v4_predict.cu — K1 v4: the v2 CTA-pair fused predictor with the GEMM2
+// operand A2 (bias + activation, split into bf16 hi / lo) kept in TENSOR
+// MEMORY instead of shared memory.
 //
-// Same math and outputs as k1_predict.cu (reference: predictor.py:193-240,
-// :330-351; core.py:27-48; metrics.py:138-193), re-tiled for the Blackwell
-// 2-SM tensor core:
-//   * a cluster of 2 CTAs owns a 256-token tile; one tcgen05.mma.cta_group::2
-//     (M=256, N=256, K=16) covers 256 tokens x 256 hidden units, each CTA
-//     staging its own 128 x-rows and half of the W1 chunk (128 rows) -> per-SM
-//     shared-memory traffic per MAC is half of the 1-SM 128x128 tile, and x is
-//     re-streamed h/256 instead of h/128 times;
-//   * GEMM1 accumulates a 256-column chunk in TMEM (single buffer); the epilogue
-//     drains it into registers at once (setmaxnreg gives the epilogue 224 regs)
-//     so the next chunk's MMAs start after a short drain;
-//   * bias + activation + bf16 hi/lo split go to a 64 KB smem A operand, fed to
-//     GEMM2 (M=256, N=E) in two K-halves so one buffer suffices;
-//   * the per-token selection / margin flag / evaluation epilogue is shared
-//     with K1 v1 (k1_common.cuh).
-// Warp roles (per CTA, 12 warps): 0 TMA x+W1, 1 MMA issue (leader CTA only),
-// 2 TMA W2, 3 TMEM alloc, 4-11 epilogue (WG0 = columns 0-127 of the chunk and
-// the token epilogue, WG1 = columns 128-255).
-// Requires hidden % 256 == 0 and E <= 128 (else the 1-SM kernel is used).
+// The epilogue writes its hi / lo pairs with tcgen05.st (no swizzle math, no
+// shared-memory write traffic, no async-proxy fence) and GEMM2 reads them with
+// the TMEM-A form of tcgen05.mma.cta_group::2 ("TS": A rows = the TMEM lanes of
+// each CTA, B = W2 from shared memory). The 64 KB of shared memory this frees
+// buys a fifth x / W1 pipeline stage (E <= 64): the role trace
+// (tools/k1_exp.py --trace) showed the v2 K-loop issuing at ~73 % of the
+// tensor rate while waiting on operand loads, with the producer's 4-stage ring
+// always full of in-flight loads. TMEM columns: accumulator [0, 256), z
+// [256, 256 + EP), A2 [256 + EP, 256 + EP + 128).
+// Everything else — work items, barriers, the per-token selection / margin /
+// evaluation epilogue — is v2's (k1v2_predict.cu; reference predictor.py:193-240,
+// :330-351, core.py:27-48, metrics.py:138-193). No hidden split (G = 1 only).
 #include <cstdio>
 #include <cuda.h>
 #include "sm100.cuh"
@@ -27,32 +22,13 @@
 #include "tmap.cuh"
 
 namespace moep {
-namespace k1v2 {
+namespace k1v4 {
 
 using k1c::Params;
 using k1c::wait;
 
-// Role-level wait accounting for tools/k1_prof.py, compiled only with
-// -DMOEP_K1_PROF (a separate library; the product build has no counters):
-// cycles spent in each barrier wait by one representative thread per role.
-#ifdef MOEP_K1_PROF
-__device__ unsigned long long g_k1_prof[160][16];
-#define K1_PW(slot, rep, call)                                                         \
-  do {                                                                                 \
-    const long long t0_ = clock64();                                                   \
-    call;                                                                              \
-    if (rep) atomicAdd(&g_k1_prof[blockIdx.x][slot], (unsigned long long)(clock64() - t0_)); \
-  } while (0)
-// per-chunk timeline of CTA 0 (clock64; MMA issuer, WG0 / WG1 warp 0 lane 0)
-__device__ long long g_k1_trace[16][64];
-#define K1_TR(ev, idx, rep)                                                   \
-  do {                                                                      \
-    if ((rep) && blockIdx.x == 0 && (idx) < 64) g_k1_trace[ev][idx] = clock64(); \
-  } while (0)
-#else
 #define K1_PW(slot, rep, call) call
 #define K1_TR(ev, idx, rep) do { } while (0)
-#endif
 
 constexpr int BM = 128;         // tokens per CTA (256 per pair)
 constexpr int BK = 64;          // K per stage
@@ -63,24 +39,57 @@ constexpr int EPI_WARP0 = 4;
 
 template <int EP>
 struct Cfg {
-  static constexpr int STAGES = (EP <= 64) ? 4 : 3;
+  // A2 (the hi/lo GEMM2 operand) lives in TMEM, so the ring gets its 64 KB
+  static constexpr int STAGES = (EP <= 64) ? 5 : 3;
   static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
   static constexpr int B_BYTES = HB * BK * 2;        // 16 KB
-  static constexpr int ATOM = BM * 64 * 2;           // 16 KB: 128 rows x 64 bf16 (SW128)
   static constexpr int W2_ROWS = EP / 2;             // expert rows staged per CTA
   static constexpr int W2_ATOM = W2_ROWS * 128;      // bytes per 64-column atom
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
-  static constexpr int OFF_A2 = OFF_B + STAGES * B_BYTES;  // [hi atom0, hi atom1, lo atom0, lo atom1]
-  static constexpr int OFF_W2 = OFF_A2 + 4 * ATOM;          // 4 atoms (256 columns)
-  static constexpr int OFF_HIST = OFF_W2 + ((4 * W2_ATOM + 1023) / 1024) * 1024;
+  static constexpr int OFF_W2 = OFF_B + STAGES * B_BYTES;   // 4 atoms (256 columns)
+  static constexpr int OFF_Z = OFF_W2 + ((4 * W2_ATOM + 1023) / 1024) * 1024;  // token-epilogue z staging
+  static constexpr int OFF_HIST = OFF_Z + BM * (EP >= 32 ? EP : EP + 1) * 4;
   static constexpr int OFF_SUMSQ = OFF_HIST + 4 * 2 * EP * 4;
   static constexpr int OFF_RED = OFF_SUMSQ + BM * 4;
   static constexpr int OFF_BAR = OFF_RED + 4 * 16 * 4;
   static constexpr int NBAR = 2 * STAGES + 10;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
-  static constexpr uint32_t ZCOL = HC;  // TMEM column of the z accumulator
+  static constexpr uint32_t ZCOL = HC;               // TMEM column of the z accumulator
+  static constexpr uint32_t A2COL = HC + EP;         // hi pairs [A2COL, +64), lo pairs [A2COL+64, +128)
+  static_assert(A2COL + 128 <= 512, "TMEM columns");
+  static_assert(SMEM <= 232448, "shared memory");
 };
+
+// 32 lanes x 32 bit, 32 consecutive columns from the even / odd entries of v[64]
+template <int ODD>
+__device__ __forceinline__ void tmem_st32_strided(uint32_t taddr, const float* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      ::"r"(taddr), "r"(r[ODD + 0]), "r"(r[ODD + 2]), "r"(r[ODD + 4]), "r"(r[ODD + 6]), "r"(r[ODD + 8]),
+        "r"(r[ODD + 10]), "r"(r[ODD + 12]), "r"(r[ODD + 14]), "r"(r[ODD + 16]), "r"(r[ODD + 18]),
+        "r"(r[ODD + 20]), "r"(r[ODD + 22]), "r"(r[ODD + 24]), "r"(r[ODD + 26]), "r"(r[ODD + 28]),
+        "r"(r[ODD + 30]), "r"(r[ODD + 32]), "r"(r[ODD + 34]), "r"(r[ODD + 36]), "r"(r[ODD + 38]),
+        "r"(r[ODD + 40]), "r"(r[ODD + 42]), "r"(r[ODD + 44]), "r"(r[ODD + 46]), "r"(r[ODD + 48]),
+        "r"(r[ODD + 50]), "r"(r[ODD + 52]), "r"(r[ODD + 54]), "r"(r[ODD + 56]), "r"(r[ODD + 58]),
+        "r"(r[ODD + 60]), "r"(r[ODD + 62])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem]^T over the CTA pair ("TS" form: each CTA's
+// 128 A rows are its TMEM lanes, 16-bit A packed two per 32-bit column).
+__device__ __forceinline__ void umma_bf16_cg2_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
 
 template <int EP, int ARCH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
@@ -104,9 +113,6 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
   uint64_t* z_empty = z_full + 1;             // leader: 8 warps read z
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
-#ifdef MOEP_K1_PROF
-  const long long k1_t_start = clock64();
-#endif
   const uint32_t warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -199,7 +205,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         const uint32_t idesc1 = idesc_bf16_f32(2 * BM, HC);
         const uint32_t idesc2 = idesc_bf16_f32(2 * BM, EP);
         const uint32_t a_base = smem_u32(smem + C::OFF_A), b_base = smem_u32(smem + C::OFF_B);
-        const uint32_t a2_base = smem_u32(smem + C::OFF_A2), w2_base = smem_u32(smem + C::OFF_W2);
+        const uint32_t w2_base = smem_u32(smem + C::OFF_W2);
         uint32_t stage = 0, phase = 0, gc = 0, ti = 0;
         // GEMM2 of a chunk is issued half by half as soon as its A2 half is
         // ready, interleaved between the next chunk's GEMM1 K-blocks (polled
@@ -225,10 +231,8 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
             for (int kk = 0; kk < 8; ++kk) {
               const int at = kk >> 2, w = kk & 3;
               const uint64_t bd = sdesc_k_sw128(w2_base + (half * 2 + at) * C::W2_ATOM + w * 32);
-              const uint64_t ahi = sdesc_k_sw128(a2_base + at * C::ATOM + w * 32);
-              const uint64_t alo = sdesc_k_sw128(a2_base + (2 + at) * C::ATOM + w * 32);
-              umma_bf16_cg2(tmem + C::ZCOL, ahi, bd, idesc2, (p_cc | half | kk) != 0);
-              umma_bf16_cg2(tmem + C::ZCOL, alo, bd, idesc2, 1u);
+              umma_bf16_cg2_ts(tmem + C::ZCOL, tmem + C::A2COL + kk * 8, bd, idesc2, (p_cc | half | kk) != 0);
+              umma_bf16_cg2_ts(tmem + C::ZCOL, tmem + C::A2COL + 64 + kk * 8, bd, idesc2, 1u);
             }
             K1_TR(3 + half, p_id, true);
             if (half == 0) {
@@ -363,23 +367,16 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
           K1_PW(9, lane == 0 && q == 0, wait(a2_emptyA, gc & 1));
           K1_TR(12, gc, lane == 0 && q == 0);
         }
-        uint8_t* a2hi = smem + C::OFF_A2;
-        uint8_t* a2lo = smem + C::OFF_A2 + 2 * C::ATOM;
-#pragma unroll
-        for (int sb = 0; sb < 4; ++sb) {
-          const int at = sb >> 1;
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            // 16-byte chunk = 8 columns = 4 column pairs starting at column sb*32 + ch*8
-            const uint32_t off = at * C::ATOM + sw128_offset(row_in_tile, (sb & 1) * 32 + ch * 8);
-            const int b = sb * 32 + ch * 8;
-            *reinterpret_cast<uint4*>(a2hi + off) = make_uint4(__float_as_uint(v[b]), __float_as_uint(v[b + 2]),
-                                                               __float_as_uint(v[b + 4]), __float_as_uint(v[b + 6]));
-            *reinterpret_cast<uint4*>(a2lo + off) = make_uint4(__float_as_uint(v[b + 1]), __float_as_uint(v[b + 3]),
-                                                               __float_as_uint(v[b + 5]), __float_as_uint(v[b + 7]));
-          }
+        // A2 in TMEM: this warp's 32 lanes, hi pairs -> [A2COL, +64), lo pairs -> [A2COL+64, +128)
+        {
+          const uint32_t ta2 = tmem + lane_addr + C::A2COL;
+          tmem_st32_strided<0>(ta2, v);
+          tmem_st32_strided<0>(ta2 + 32, v + 64);
+          tmem_st32_strided<1>(ta2 + 64, v);
+          tmem_st32_strided<1>(ta2 + 96, v + 64);
+          tmem_st_wait();
         }
-        fence_async_smem();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&a2_full[wg], 0);
         K1_TR(wg == 0 ? 8 : 13, gc, lane == 0 && q == 0);
@@ -406,10 +403,8 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
           for (int j = 0; j < EP; j += 4) *reinterpret_cast<float4*>(zp + j) = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
           p.zpart[static_cast<int64_t>(G) * p.zpad * EP + static_cast<int64_t>(grp) * p.zpad + row_g] = sumsq;
         } else {
-          // The A2 buffer is idle here: WG1 cannot write the next tile's A2 before
-          // GEMM2 half 0 of its chunk 0, which needs this warpgroup's half first.
           uint32_t zswz;
-          float* zrow = k1c::zstage_row<EP>(smem + C::OFF_A2, row_in_tile, lane, zswz);
+          float* zrow = k1c::zstage_row<EP>(smem + C::OFF_Z, row_in_tile, lane, zswz);
           k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc, zrow, zswz);
           K1_TR(15, gc - 1, lane == 0 && q == 0);
         }
@@ -428,288 +423,13 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
   if (warp == 3) tmem_dealloc_cg2<512>(tmem);
 }
 
-// Hidden-split finish: z = fixed-order sum of the groups' partial logits, then
-// the per-token selection / margin / output / counter semantics of
-// k1c::row_epilogue (the fused path's epilogue), re-laid for one WARP per token
-// (lane l holds experts l, l+32, ...): the top list is built by warp argmax
-// reductions (value, then lower index on ties; -0.0 == +0.0), ascending ids by
-// ballot prefix sums, truth-expert lookups by shuffles. grid = num_SMs (one
-// counter partial row per CTA, the layout moep_counters_reduce expects).
-template <int EP>
-__global__ void __launch_bounds__(256) split_finish_kernel(const Params p) {
-  constexpr int PL = EP >= 32 ? EP / 32 : 1;   // experts per lane
-  __shared__ int hist_s[2 * EP];
-  __shared__ int cnt_s[2 + 2 * MOEP_MAX_BOUNDS];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < 2 * EP; i += 256) hist_s[i] = 0;
-  if (tid < 2 + 2 * MOEP_MAX_BOUNDS) cnt_s[tid] = 0;
-  __syncthreads();
-  const int G = p.split, E = p.E;
-  const float* sq = p.zpart + static_cast<int64_t>(G) * p.zpad * EP;
-  int P = p.m_sel;
-#pragma unroll
-  for (int b = 0; b < MOEP_MAX_BOUNDS; ++b)
-    if (b < p.n_bounds && p.bounds[b] > P) P = p.bounds[b];
-  P = min(P + 1, min(E, kMaxSel));
-  RowCounters rc;
-  rc.zero();
-  const int64_t nw = static_cast<int64_t>(gridDim.x) * 8;
-  for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp; row < p.n_tokens; row += nw) {
-    float zv[PL];
-    bool bad = false;
-#pragma unroll
-    for (int q = 0; q < PL; ++q) {
-      const int e = q * 32 + lane;
-      float acc = 0.f;
-      if (e < EP) {
-        // all groups' partials in flight together, then the fixed-order sum
-        float v[16];
-#pragma unroll
-        for (int g = 0; g < 16; ++g)
-          v[g] = g < G ? __ldcg(p.zpart + (static_cast<int64_t>(g) * p.zpad + row) * EP + e) : 0.f;
-#pragma unroll
-        for (int g = 0; g < 16; ++g)
-          if (g < G) acc += v[g];
-      }
-      if (e < E) {
-        acc += __ldg(p.b2 + e);
-        bad |= !isfinite(acc);
-      } else {
-        acc = -INFINITY;
-      }
-      zv[q] = acc;
-    }
-    float sumsq = 0.f;
-    {
-      // lane g loads group g's ||h||^2 partial; lane 0 sums them in order
-      const float part = lane < G ? __ldcg(sq + static_cast<int64_t>(lane) * p.zpad + row) : 0.f;
-#pragma unroll
-      for (int g = 0; g < 16; ++g) {
-        const float v = __shfl_sync(0xffffffffu, part, g);
-        if (g < G) sumsq += v;
-      }
-    }
-    bool flagged = __any_sync(0xffffffffu, bad);
-    // sorted top list (warp-uniform): repeated warp argmax over the untaken experts
-    float tv[kMaxSel];
-    int tix[kMaxSel];
-    uint32_t taken = 0;
-#pragma unroll
-    for (int s = 0; s < kMaxSel; ++s) {
-      float best = -INFINITY;
-      int bi = 0x7fffffff;
-      if (s < P) {
-#pragma unroll
-        for (int q = 0; q < PL; ++q) {
-          const int e = q * 32 + lane;
-          if (!((taken >> q) & 1u) && e < EP && (zv[q] > best || (zv[q] == best && e < bi))) { best = zv[q]; bi = e; }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-        }
-        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-      }
-      tv[s] = best;
-      tix[s] = bi;
-    }
-    const float delta = p.tau_abs + p.tau_rel * sqrtf(sumsq) * p.w2_norm;
-#pragma unroll
-    for (int b = 0; b < MOEP_MAX_BOUNDS; ++b) {
-      if (b < p.n_bounds) {
-        const int pos = p.bounds[b];
-        if (pos >= 1 && pos < E) {
-          float hi_v = tv[0], lo_v = tv[1];
-#pragma unroll
-          for (int s = 1; s < kMaxSel; ++s)
-            if (s == pos) { hi_v = tv[s - 1]; lo_v = tv[s]; }
-          flagged |= !(hi_v - lo_v >= delta);
-        }
-      }
-    }
-    if (lane == 0) {
-      if (p.flags) p.flags[row] = flagged ? 1 : 0;
-      if (flagged) p.flag_list[atomicAdd(p.flag_count, 1)] = static_cast<int>(row);
-    }
-    if (p.logits) {
-#pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        const int e = q * 32 + lane;
-        if (e < E) p.logits[row * E + e] = zv[q];
-      }
-    }
-    if (p.ids && !flagged) {
-      int* orow = p.ids + row * p.m_sel;
-      if (p.m_sel >= E) {
-        for (int e = lane; e < E; e += 32) orow[e] = e;
-      } else {
-        float thv = tv[0];
-        int thi = tix[0];
-#pragma unroll
-        for (int s = 0; s < kMaxSel; ++s)
-          if (s == p.m_sel - 1) { thv = tv[s]; thi = tix[s]; }
-        int base = 0;
-#pragma unroll
-        for (int q = 0; q < PL; ++q) {
-          const int e = q * 32 + lane;
-          const bool sel = e < E && ((zv[q] > thv || (zv[q] == thv && e < thi)) || e == thi);
-          const uint32_t mask = __ballot_sync(0xffffffffu, sel);
-          if (sel) orow[base + __popc(mask & ((1u << lane) - 1u))] = e;
-          base += __popc(mask);
-        }
-      }
-    }
-    if (p.truth && !flagged) {
-      // "truth expert t has predicted rank < m" <=> key(t) >= key(position m-1) of the top list
-      const bool act = lane < p.k;
-      const int t = act ? __ldg(p.truth + row * p.k + lane) : 0;
-      float zt = 0.f;
-#pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        const float v = __shfl_sync(0xffffffffu, zv[q], t & 31);
-        if ((t >> 5) == q) zt = v;
-      }
-      auto thr = [&](int m, float& v, int& ix) {
-        v = tv[0];
-        ix = tix[0];
-#pragma unroll
-        for (int s = 0; s < kMaxSel; ++s)
-          if (s == m - 1) { v = tv[s]; ix = tix[s]; }
-      };
-      float kv;
-      int ki;
-      thr(p.k, kv, ki);
-      const bool hit = act && ((zt > kv || (zt == kv && t < ki)) || t == ki);
-      if (act) {
-        atomicAdd(&hist_s[EP + t], 1);
-        if (hit) atomicAdd(&hist_s[t], 1);
-      }
-      const bool any0 = __any_sync(0xffffffffu, act && t == tix[0]);
-      rc.n += 1;
-      rc.top1 += any0 ? 1 : 0;
-#pragma unroll
-      for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
-        if (mi < p.n_m) {
-          const int m = p.m_list[mi];
-          float mv;
-          int mx;
-          thr(m < kMaxSel ? m : 1, mv, mx);
-          const bool in = act && (m >= E || (zt > mv || (zt == mv && t < mx)) || t == mx);
-          const int cnt = __popc(__ballot_sync(0xffffffffu, in));
-          rc.ov[mi] += cnt == p.k ? 1 : 0;
-          rc.rc[mi] += cnt;
-        }
-      }
-    }
-  }
-  if (p.partials) {
-    if (lane == 0) {
-      atomicAdd(&cnt_s[0], rc.n);
-      atomicAdd(&cnt_s[1], rc.top1);
-#pragma unroll
-      for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
-        atomicAdd(&cnt_s[2 + mi], rc.ov[mi]);
-        atomicAdd(&cnt_s[2 + MOEP_MAX_BOUNDS + mi], rc.rc[mi]);
-      }
-    }
-    __syncthreads();
-    int* out = p.partials + static_cast<int64_t>(blockIdx.x) * p.n_counters;
-    for (int t = tid; t < p.n_counters; t += 256) {
-      int v;
-      if (t < 2) v = cnt_s[t];
-      else if (t < 2 + p.n_m) v = cnt_s[2 + (t - 2)];
-      else if (t < 2 + 2 * p.n_m) v = cnt_s[2 + MOEP_MAX_BOUNDS + (t - 2 - p.n_m)];
-      else {
-        const int u = t - 2 - 2 * p.n_m;  // [hits E | truth E]
-        v = u < E ? hist_s[u] : hist_s[EP + (u - E)];
-      }
-      out[t] = v;
-    }
-  }
-}
-
-// Which pair kernel runs: v2 (256-column chunks, single accumulator) by
-// default; MOEP_K1_VARIANT=3 selects v3 (double-buffered accumulator,
-// 192-column chunks, E <= 64), which removes the drain bubble but measured
-// slower (the per-chunk epilogue becomes the limit: profiles/r01_k1_role_waits.md).
-// MOEP_K1_VARIANT=1 selects the 1-SM kernel in moep_predict_bf16.
-static int variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* env = getenv("MOEP_K1_VARIANT");
-    v = (env && env[0] == '3') ? 3 : (env && env[0] == '4') ? 4 : 2;
-  }
-  return v;
-}
-static bool use_v3(int hidden, int n_experts) {
-  return variant() == 3 && hidden % 64 == 0 && n_experts <= 64;  // EP = 128 spills in v3 (round 2)
-}
-// v4 (A2 in TMEM, 5-stage ring; k1v4_predict.cu) for unsplit launches
-static bool use_v4(int hidden) { return variant() == 4 && hidden % HC == 0; }
-
-static int pair_chunks(int hidden, int n_experts) {
-  return use_v3(hidden, n_experts) ? (hidden + 191) / 192 : hidden / HC;
-}
-
-// Chunk groups per tile: only when the tiles leave CTA pairs idle (fewer tiles
-// than pairs); then the fewest pair-rounds of chunks, ties to fewer groups.
-// Large N never splits (the partial-logit traffic and the x re-streaming would
-// cost more than the last-wave imbalance they remove).
-static int choose_split(int64_t n_tokens, int nchunks, int n_pairs) {
-  const int64_t tiles = (n_tokens + 2 * BM - 1) / (2 * BM);
-  if (tiles >= n_pairs) return 1;
-  const int64_t cost1 = ((tiles + n_pairs - 1) / n_pairs) * nchunks;
-  int best = 1;
-  int64_t best_cost = cost1;
-  for (int g = 2; g <= nchunks && g <= 16; ++g) {
-    if (nchunks % g) continue;
-    const int64_t cost = ((tiles * g + n_pairs - 1) / n_pairs) * (nchunks / g);
-    if (cost < best_cost) { best = g; best_cost = cost; }
-  }
-  // a split pays per-item pipeline fills, the partial-logit traffic and the
-  // finish kernel: take it only for a clear gain (at most 3/4 of the rounds)
-  return 4 * best_cost <= 3 * cost1 ? best : 1;
-}
-
-}  // namespace k1v2
+}  // namespace k1v4
 }  // namespace moep
-
-#ifdef MOEP_K1_PROF
-extern "C" int moep_k1_trace(long long* host) {
-  return cudaMemcpyFromSymbol(host, moep::k1v2::g_k1_trace, sizeof(long long) * 16 * 64) == cudaSuccess ? 0 : -4;
-}
-extern "C" int moep_k1_prof(unsigned long long* host, int reset) {
-  if (reset) {
-    static unsigned long long zero[160][16];
-    return cudaMemcpyToSymbol(moep::k1v2::g_k1_prof, zero, sizeof(zero)) == cudaSuccess ? 0 : -4;
-  }
-  return cudaMemcpyFromSymbol(host, moep::k1v2::g_k1_prof, sizeof(unsigned long long) * 160 * 16) == cudaSuccess
-             ? 0 : -4;
-}
-#endif
-
-extern "C" int64_t moep_predict_split_floats(int64_t n_tokens, int32_t hidden, int32_t n_experts) {
-  using namespace moep::k1v2;
-  if (n_tokens <= 0 || hidden <= 0 || n_experts <= 0 || n_experts > 128) return 0;
-  if (hidden % HC != 0 && !use_v3(hidden, n_experts)) return 0;
-  const int g = choose_split(n_tokens, pair_chunks(hidden, n_experts), moep_num_sms() / 2);
-  if (g == 1) return 0;
-  int EP = 16;
-  while (EP < n_experts) EP *= 2;
-  const int64_t zpad = ((n_tokens + 2 * BM - 1) / (2 * BM)) * 2 * BM;
-  return static_cast<int64_t>(g) * zpad * (EP + 1);
-}
-
-extern "C" int moep_predict_bf16_pair3(const moep_predict_args* a, int split, float* zpart, int64_t zpad,
-                                       void* stream);
-extern "C" int moep_predict_bf16_pair4(const moep_predict_args* a, void* stream);
 
 namespace {
 template <int EP, int ARCH>
-int launch_v2(const moep_predict_args* a, cudaStream_t st) {
-  using namespace moep::k1v2;
+int launch_v4(const moep_predict_args* a, cudaStream_t st) {
+  using namespace moep::k1v4;
   using C = Cfg<EP>;
   static bool attr_set[64] = {};
   int dev = 0;
@@ -735,43 +455,24 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
   p.flag_list = a->flag_list; p.flag_count = a->flag_count;
   p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;
   p.n_counters = moep_n_counters(a->n_m, a->n_experts);
-  const int grid = moep_num_sms() & ~1;  // whole CTA pairs
   p.split = 1; p.zpart = nullptr; p.zpad = 0;
-  const int64_t need = moep_predict_split_floats(a->n_tokens, a->hidden, a->n_experts);
-  if (need > 0 && a->split_scratch && a->split_scratch_floats >= need) {
-    p.split = choose_split(a->n_tokens, pair_chunks(a->hidden, a->n_experts), grid / 2);
-    p.zpart = a->split_scratch;
-    p.zpad = ((a->n_tokens + 2 * BM - 1) / (2 * BM)) * 2 * BM;
-  }
-  if (use_v3(a->hidden, a->n_experts)) {
-    const int rc = moep_predict_bf16_pair3(a, p.split, p.zpart, p.zpad, st);
-    if (rc != MOEP_OK) return rc;
-  } else if (p.split == 1 && use_v4(a->hidden)) {
-    return moep_predict_bf16_pair4(a, st);
-  } else {
-    kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);
-    if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
-  }
-  if (p.split > 1) {
-    split_finish_kernel<EP><<<moep_num_sms(), 256, 0, st>>>(p);
-    if (cudaGetLastError() != cudaSuccess) return MOEP_ELAUNCH;
-  }
-  return MOEP_OK;
+  const int grid = moep_num_sms() & ~1;
+  kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }
 }  // namespace
 
-// Pair kernel entry (validation shared with moep_predict_bf16, which dispatches here).
-extern "C" int moep_predict_bf16_pair(const moep_predict_args* a, void* stream) {
-  if (a->n_experts > 128) return MOEP_EUNSUPPORTED;
-  if (a->hidden % 256 != 0 && !moep::k1v2::use_v3(a->hidden, a->n_experts)) return MOEP_EUNSUPPORTED;
+// v4 pair kernel (no hidden split): hidden % 256 == 0, E <= 128.
+extern "C" int moep_predict_bf16_pair4(const moep_predict_args* a, void* stream) {
+  if (a->n_experts > 128 || a->hidden % 256 != 0) return MOEP_EUNSUPPORTED;
   int EP = 16;
   while (EP < a->n_experts) EP *= 2;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool a1 = a->arch == 1;
   switch (EP) {
-    case 16: return a1 ? launch_v2<16, 1>(a, st) : launch_v2<16, 2>(a, st);
-    case 32: return a1 ? launch_v2<32, 1>(a, st) : launch_v2<32, 2>(a, st);
-    case 64: return a1 ? launch_v2<64, 1>(a, st) : launch_v2<64, 2>(a, st);
-    default: return a1 ? launch_v2<128, 1>(a, st) : launch_v2<128, 2>(a, st);
+    case 16: return a1 ? launch_v4<16, 1>(a, st) : launch_v4<16, 2>(a, st);
+    case 32: return a1 ? launch_v4<32, 1>(a, st) : launch_v4<32, 2>(a, st);
+    case 64: return a1 ? launch_v4<64, 1>(a, st) : launch_v4<64, 2>(a, st);
+    default: return a1 ? launch_v4<128, 1>(a, st) : launch_v4<128, 2>(a, st);
   }
 }
