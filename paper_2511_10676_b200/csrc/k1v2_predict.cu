@@ -630,24 +630,26 @@ __global__ void __launch_bounds__(256) split_finish_kernel(const Params p) {
   }
 }
 
-// Which pair kernel runs: v2 (256-column chunks, single accumulator) by
-// default; MOEP_K1_VARIANT=3 selects v3 (double-buffered accumulator,
-// 192-column chunks, E <= 64), which removes the drain bubble but measured
-// slower (the per-chunk epilogue becomes the limit: profiles/r01_k1_role_waits.md).
-// MOEP_K1_VARIANT=1 selects the 1-SM kernel in moep_predict_bf16.
+// Which pair kernel runs: v4 (k1v4_predict.cu: token epilogue on its own
+// warpgroup, A2 in TMEM) for unsplit launches with E <= 64, this file's v2
+// kernel otherwise (E = 128, hidden-split small-N launches).
+// MOEP_K1_VARIANT=2 forces v2; =3 selects v3 (double-buffered accumulator,
+// 192-column chunks, E <= 64: removes the drain bubble but measured slower,
+// profiles/r01_k1_role_waits.md); =1 selects the 1-SM kernel in moep_predict_bf16.
 static int variant() {
   static int v = -1;
   if (v < 0) {
     const char* env = getenv("MOEP_K1_VARIANT");
-    v = (env && env[0] == '3') ? 3 : (env && env[0] == '4') ? 4 : 2;
+    v = (env && env[0] == '3') ? 3 : (env && env[0] == '2') ? 2 : 4;
   }
   return v;
 }
 static bool use_v3(int hidden, int n_experts) {
   return variant() == 3 && hidden % 64 == 0 && n_experts <= 64;  // EP = 128 spills in v3 (round 2)
 }
-// v4 (A2 in TMEM, 5-stage ring; k1v4_predict.cu) for unsplit launches
-static bool use_v4(int hidden) { return variant() == 4 && hidden % HC == 0; }
+// v4 (A2 in TMEM, 5-stage ring, token epilogue on its own warpgroup;
+// k1v4_predict.cu) for unsplit launches with E <= 64 (E = 128 spills there)
+static bool use_v4(int hidden, int n_experts) { return variant() == 4 && hidden % HC == 0 && n_experts <= 64; }
 
 static int pair_chunks(int hidden, int n_experts) {
   return use_v3(hidden, n_experts) ? (hidden + 191) / 192 : hidden / HC;
@@ -746,7 +748,7 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
   if (use_v3(a->hidden, a->n_experts)) {
     const int rc = moep_predict_bf16_pair3(a, p.split, p.zpart, p.zpad, st);
     if (rc != MOEP_OK) return rc;
-  } else if (p.split == 1 && use_v4(a->hidden)) {
+  } else if (p.split == 1 && use_v4(a->hidden, a->n_experts)) {
     return moep_predict_bf16_pair4(a, st);
   } else {
     kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);

@@ -1,6 +1,18 @@
-// k1v4_predict.cu — K1 v4: the v2 CTA-pair fused predictor with the GEMM2
-// operand A2 (bias + activation, split into bf16 hi / lo) kept in TENSOR
+// k1v4_predict.cu — K1 v4 (default for E <= 64): the v2 CTA-pair fused
+// predictor with (1) the per-token epilogue on its own warpgroup and (2) the
+// GEMM2 operand A2 (bias + activation, split into bf16 hi / lo) kept in TENSOR
 // MEMORY instead of shared memory.
+//
+// (1) v2 ran the per-token selection / margin / counter epilogue on the
+// warpgroup that also drains the accumulator; for ~66 k cycles per tile it
+// could not drain the next tile's first chunk and the tensor pipe stalled
+// (per-chunk trace: every 8th chunk took ~75 k cycles instead of 27 k). Here
+// WG2 (warps 12-15) owns z: it reads the tile's z from TMEM (the MMA waits
+// only for that read, z_empty), takes the two ||h||^2 partials from WG0 / WG1
+// through a double-buffered shared-memory hand-off (sum_ready / sum_empty) and
+// runs the selection while the next tile's chunks stream. Chunk period
+// 27.1 k -> 22.4 k cycles, no per-tile stall. 512 threads: setmaxnreg splits
+// the register file 72 (TMA / MMA warps) / 160 (chunk epilogue) / 120 (WG2).
 //
 // The epilogue writes its hi / lo pairs with tcgen05.st (no swizzle math, no
 // shared-memory write traffic, no async-proxy fence) and GEMM2 reads them with
@@ -28,14 +40,33 @@ using k1c::Params;
 using k1c::wait;
 
 #define K1_PW(slot, rep, call) call
+#ifdef MOEP_K1_PROF
+// per-chunk timeline of CTA 0 (tools/k1_exp.py --trace), same events as v2
+__device__ long long g_k1v4_trace[16][64];
+#define K1_TR(ev, idx, rep)                                                      \
+  do {                                                                         \
+    if ((rep) && blockIdx.x == 0 && (idx) < 64) g_k1v4_trace[ev][idx] = clock64(); \
+  } while (0)
+#else
 #define K1_TR(ev, idx, rep) do { } while (0)
+#endif
 
 constexpr int BM = 128;         // tokens per CTA (256 per pair)
 constexpr int BK = 64;          // K per stage
 constexpr int HC = 256;         // hidden columns per chunk (pair MMA N)
 constexpr int HB = HC / 2;      // W1 rows staged per CTA
-constexpr int NTHREADS = 384;
-constexpr int EPI_WARP0 = 4;
+constexpr int NTHREADS = 512;
+constexpr int EPI_WARP0 = 4;   // WG0 = warps 4-7, WG1 = warps 8-11 (chunk epilogue)
+constexpr int TOK_WARP0 = 12;  // WG2 = warps 12-15 (per-token epilogue)
+// register split (setmaxnreg; 128 per thread at launch): 4 warps x PROD +
+// 8 x EPI + 4 x WG2 <= 16 x 128
+#ifndef K1V4_PROD_REGS
+#define K1V4_PROD_REGS 72
+#define K1V4_EPI_REGS 160
+#define K1V4_WG2_REGS 120
+#endif
+constexpr int PROD_REGS = K1V4_PROD_REGS, EPI_REGS = K1V4_EPI_REGS, WG2_REGS = K1V4_WG2_REGS;
+static_assert(PROD_REGS + 2 * EPI_REGS + WG2_REGS <= 4 * 128, "register pool");
 
 template <int EP>
 struct Cfg {
@@ -51,9 +82,9 @@ struct Cfg {
   static constexpr int OFF_Z = OFF_W2 + ((4 * W2_ATOM + 1023) / 1024) * 1024;  // token-epilogue z staging
   static constexpr int OFF_HIST = OFF_Z + BM * (EP >= 32 ? EP : EP + 1) * 4;
   static constexpr int OFF_SUMSQ = OFF_HIST + 4 * 2 * EP * 4;
-  static constexpr int OFF_RED = OFF_SUMSQ + BM * 4;
+  static constexpr int OFF_RED = OFF_SUMSQ + 2 * 2 * BM * 4;
   static constexpr int OFF_BAR = OFF_RED + 4 * 16 * 4;
-  static constexpr int NBAR = 2 * STAGES + 10;
+  static constexpr int NBAR = 2 * STAGES + 14;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
   static constexpr uint32_t ZCOL = HC;               // TMEM column of the z accumulator
   static constexpr uint32_t A2COL = HC + EP;         // hi pairs [A2COL, +64), lo pairs [A2COL+64, +128)
@@ -110,7 +141,9 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
   uint64_t* w2_full = a2_emptyB + 1;          // leader: W2 chunk of both CTAs landed
   uint64_t* w2_empty = w2_full + 1;           // local
   uint64_t* z_full = w2_empty + 1;            // local
-  uint64_t* z_empty = z_full + 1;             // leader: 8 warps read z
+  uint64_t* z_empty = z_full + 1;             // leader: WG2's 8 warps (both CTAs) read z
+  uint64_t* sum_ready = z_empty + 1;          // [2] local: WG0 + WG1 wrote the tile's ||h||^2 partials
+  uint64_t* sum_empty = sum_ready + 2;        // [2] local: WG2 read them
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -136,6 +169,10 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
     mbar_init(w2_empty, 1);
     mbar_init(z_full, 1);
     mbar_init(z_empty, 8);
+    mbar_init(&sum_ready[0], 8);
+    mbar_init(&sum_ready[1], 8);
+    mbar_init(&sum_empty[0], 4);
+    mbar_init(&sum_empty[1], 4);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -148,6 +185,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
   const uint32_t tmem = *tmem_slot;
 
   if (warp < EPI_WARP0) {
+    regs_dec<PROD_REGS>();
     if (warp == 0) {
       // ---------------------------------------------- TMA: x rows + W1 half-chunk
       if (elect_one()) {
@@ -273,19 +311,14 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         pump(true);
       }
     }
-  } else {
-    // ------------------------------------------------ epilogue warpgroups
+  } else if (warp < TOK_WARP0) {
+    // ------------------------------------------------ chunk epilogue warpgroups
+    regs_inc<EPI_REGS>();
     const int wg = (warp - EPI_WARP0) >> 2;  // 0: chunk columns 0-127, 1: 128-255
     const uint32_t q = warp & 3;
     const int row_in_tile = q * 32 + lane;
     const uint32_t lane_addr = (q * 32) << 16;
     float* s_sumsq = reinterpret_cast<float*>(smem + C::OFF_SUMSQ);
-    int* hist0 = reinterpret_cast<int*>(smem + C::OFF_HIST);
-    int* hist = hist0 + q * 2 * EP;
-    if (wg == 0)
-      for (int e = lane; e < 2 * EP; e += 32) hist[e] = 0;
-    RowCounters rc;
-    rc.zero();
     uint32_t gc = 0, ti = 0;
     for (int item = pair; item < n_items; item += n_pairs, ++ti) {
       const int tile = item / G, grp = item % G, c0 = grp * cpg;
@@ -294,9 +327,6 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       for (int c = c0; c < c0 + cpg; ++c, ++gc) {
         K1_PW(wg == 0 ? 7 : 11, lane == 0 && q == 0, wait(acc_full, gc & 1));
         K1_TR(wg == 0 ? 5 : 9, gc, lane == 0 && q == 0);
-#ifdef MOEP_K1_PROF
-        const long long t_drain0 = clock64();
-#endif
         tc_fence_after();
         float v[128];
         const uint32_t ta = tmem + lane_addr + wg * 128;
@@ -309,11 +339,6 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(acc_empty, 0);
         K1_TR(wg == 0 ? 6 : 10, gc, lane == 0 && q == 0);
-#ifdef MOEP_K1_PROF
-        if (lane == 0 && q == 0)
-          atomicAdd(&g_k1_prof[blockIdx.x][wg == 0 ? 12 : 13], (unsigned long long)(clock64() - t_drain0));
-        const long long t_conv0 = clock64();
-#endif
         // bias + activation + hi/lo split, in place per column pair (2j, 2j+1):
         // v[2j] <- packed bf16x2 hi, v[2j+1] <- packed bf16x2 lo
         const int col0 = c * HC + wg * 128;
@@ -355,10 +380,6 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
             v[j4 * 4 + t + 1] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&lp));
           }
         }
-#ifdef MOEP_K1_PROF
-        if (lane == 0 && q == 0) atomicAdd(&g_k1_prof[blockIdx.x][wg == 0 ? 14 : 3], 0ull);
-        if (lane == 0 && q == 0 && wg == 0) atomicAdd(&g_k1_prof[blockIdx.x][14], (unsigned long long)(clock64() - t_conv0));
-#endif
         K1_TR(wg == 0 ? 7 : 11, gc, lane == 0 && q == 0);
         // the A2 buffer is free once the previous GEMM2 half that read it completed
         if (wg == 0) {
@@ -381,44 +402,57 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
         if (lane == 0) mbar_arrive_remote(&a2_full[wg], 0);
         K1_TR(wg == 0 ? 8 : 13, gc, lane == 0 && q == 0);
       }
-      // ---- token epilogue on warpgroup 0
-      if (wg == 1) s_sumsq[row_in_tile] = sumsq;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (wg == 0) {
-        sumsq += s_sumsq[row_in_tile];
-        K1_PW(10, lane == 0 && q == 0, wait(z_full, ti & 1));
-        K1_TR(14, gc - 1, lane == 0 && q == 0);
-        tc_fence_after();
-        float z[EP];
-#pragma unroll
-        for (int j = 0; j < EP; j += 16) tmem_ld16(tmem + lane_addr + C::ZCOL + j, z + j);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote(z_empty, 0);
-        if (G > 1) {
-          // hidden split: this group's partial z and ||h||^2 (split_finish sums the groups)
-          float* zp = p.zpart + (static_cast<int64_t>(grp) * p.zpad + row_g) * EP;
-#pragma unroll
-          for (int j = 0; j < EP; j += 4) *reinterpret_cast<float4*>(zp + j) = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
-          p.zpart[static_cast<int64_t>(G) * p.zpad * EP + static_cast<int64_t>(grp) * p.zpad + row_g] = sumsq;
-        } else {
-          uint32_t zswz;
-          float* zrow = k1c::zstage_row<EP>(smem + C::OFF_Z, row_in_tile, lane, zswz);
-          k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc, zrow, zswz);
-          K1_TR(15, gc - 1, lane == 0 && q == 0);
-        }
-      }
+      // ---- hand this tile's ||h||^2 partial to WG2 (double-buffered by tile parity)
+      if (ti >= 2) wait(&sum_empty[ti & 1], ((ti >> 1) & 1) ^ 1);
+      s_sumsq[((ti & 1) * 2 + wg) * BM + row_in_tile] = sumsq;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sum_ready[ti & 1]);
     }
-    if (wg == 0 && p.partials && G == 1)
-      k1c::write_partials<EP>(p, rc, q, lane, threadIdx.x - EPI_WARP0 * 32,
+  } else {
+    // ------------------------------------------------ WG2: per-token epilogue
+    regs_dec<WG2_REGS>();
+    // Owns z, the selection / margin / ids / counters of each tile, off the
+    // chunk pipeline: the MMA only waits for WG2's z read (z_empty) before the
+    // next tile's first GEMM2, not for the selection work.
+    const uint32_t q = warp & 3;
+    const int row_in_tile = q * 32 + lane;
+    const uint32_t lane_addr = (q * 32) << 16;
+    const float* s_sumsq = reinterpret_cast<const float*>(smem + C::OFF_SUMSQ);
+    int* hist0 = reinterpret_cast<int*>(smem + C::OFF_HIST);
+    int* hist = hist0 + q * 2 * EP;
+    for (int e = lane; e < 2 * EP; e += 32) hist[e] = 0;
+    RowCounters rc;
+    rc.zero();
+    uint32_t ti = 0;
+    for (int item = pair; item < n_items; item += n_pairs, ++ti) {
+      const int tile = item;
+      const int64_t row_g = static_cast<int64_t>(tile) * 2 * BM + rank * BM + row_in_tile;
+      wait(z_full, ti & 1);
+      K1_TR(14, ti * 8 + 7, lane == 0 && q == 0);
+      tc_fence_after();
+      float z[EP];
+#pragma unroll
+      for (int j = 0; j < EP; j += 16) tmem_ld16(tmem + lane_addr + C::ZCOL + j, z + j);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(z_empty, 0);
+      wait(&sum_ready[ti & 1], (ti >> 1) & 1);
+      const float sumsq = s_sumsq[((ti & 1) * 2 + 0) * BM + row_in_tile] +
+                          s_sumsq[((ti & 1) * 2 + 1) * BM + row_in_tile];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sum_empty[ti & 1]);
+      uint32_t zswz;
+      float* zrow = k1c::zstage_row<EP>(smem + C::OFF_Z, row_in_tile, lane, zswz);
+      k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc, zrow, zswz);
+      K1_TR(15, ti * 8 + 7, lane == 0 && q == 0);
+    }
+    if (p.partials)
+      k1c::write_partials<EP>(p, rc, q, lane, threadIdx.x - TOK_WARP0 * 32,
                               reinterpret_cast<int*>(smem + C::OFF_RED), hist0, 2);
   }
   tc_fence_before();
   __syncthreads();
-#ifdef MOEP_K1_PROF
-  if (threadIdx.x == 0) atomicAdd(&g_k1_prof[blockIdx.x][15], (unsigned long long)(clock64() - k1_t_start));
-#endif
   cluster_sync();
   if (warp == 3) tmem_dealloc_cg2<512>(tmem);
 }
@@ -462,9 +496,15 @@ int launch_v4(const moep_predict_args* a, cudaStream_t st) {
 }
 }  // namespace
 
-// v4 pair kernel (no hidden split): hidden % 256 == 0, E <= 128.
+#ifdef MOEP_K1_PROF
+extern "C" int moep_k1v4_trace(long long* host) {
+  return cudaMemcpyFromSymbol(host, moep::k1v4::g_k1v4_trace, sizeof(long long) * 16 * 64) == cudaSuccess ? 0 : -4;
+}
+#endif
+
+// v4 pair kernel (no hidden split): hidden % 256 == 0, E <= 64.
 extern "C" int moep_predict_bf16_pair4(const moep_predict_args* a, void* stream) {
-  if (a->n_experts > 128 || a->hidden % 256 != 0) return MOEP_EUNSUPPORTED;
+  if (a->n_experts > 64 || a->hidden % 256 != 0) return MOEP_EUNSUPPORTED;
   int EP = 16;
   while (EP < a->n_experts) EP *= 2;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -473,6 +513,6 @@ extern "C" int moep_predict_bf16_pair4(const moep_predict_args* a, void* stream)
     case 16: return a1 ? launch_v4<16, 1>(a, st) : launch_v4<16, 2>(a, st);
     case 32: return a1 ? launch_v4<32, 1>(a, st) : launch_v4<32, 2>(a, st);
     case 64: return a1 ? launch_v4<64, 1>(a, st) : launch_v4<64, 2>(a, st);
-    default: return a1 ? launch_v4<128, 1>(a, st) : launch_v4<128, 2>(a, st);
+    default: return MOEP_EUNSUPPORTED;  // E = 128: WG2's z[128] spills at its register share; v2 runs it
   }
 }

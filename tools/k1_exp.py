@@ -52,8 +52,9 @@ for _ in range(3): run()
 torch.cuda.synchronize()
 run(); torch.cuda.synchronize()
 buf = np.zeros((16, 64), dtype=np.int64)
-L.moep_k1_trace.argtypes = [C.c_void_p]
-L.moep_k1_trace(buf.ctypes.data)
+fn = L.moep_k1v4_trace if os.environ.get("MOEP_K1_VARIANT") == "4" else L.moep_k1_trace
+fn.argtypes = [C.c_void_p]
+fn(buf.ctypes.data)
 print(json.dumps(buf.tolist()))
 ''' % ROOT
 
@@ -88,13 +89,17 @@ def build(tag):
     from paper_2511_10676_b200 import build as b
     b.build()
     os.makedirs(OUT, exist_ok=True)
-    obj = os.path.join(OUT, f"k1v2_{tag}.o")
     lib = os.path.join(OUT, f"libmoep_exp_{tag}.so")
-    src = os.path.join(b.CSRC, "k1v2_predict.cu")
-    subprocess.run([b.nvcc(), *b.ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *FLAGS[tag],
-                    "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj], check=True)
-    others = [o for o in glob.glob(os.path.join(b.HERE, "_build", "*.o")) if not o.endswith("k1v2_predict.o")]
-    subprocess.run([b.nvcc(), *b.ARCH, "-shared", "-o", lib, obj, *others], check=True)
+    objs = []
+    for name in ("k1v2_predict", "k1v4_predict"):
+        obj = os.path.join(OUT, f"{name}_{tag}.o")
+        subprocess.run([b.nvcc(), *b.ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *FLAGS[tag],
+                        "-I", os.path.join(ROOT, "include"), "-c", os.path.join(b.CSRC, name + ".cu"), "-o", obj],
+                       check=True)
+        objs.append(obj)
+    others = [o for o in glob.glob(os.path.join(b.HERE, "_build", "*.o"))
+              if not o.endswith(("k1v2_predict.o", "k1v4_predict.o"))]
+    subprocess.run([b.nvcc(), *b.ARCH, "-shared", "-o", lib, *objs, *others], check=True)
     return lib
 
 
