@@ -119,6 +119,14 @@ __device__ __forceinline__ void row_epilogue(const Params& p, float* z, float su
     }
   }
   const float delta = p.tau_abs + p.tau_rel * sqrtf(sumsq) * p.w2_norm;
+  // Near-tie margin. Every logit is within delta/2 of its exact value, so the
+  // top-`pos` set can only change when the boundary gap v[pos-1] - v[pos] is
+  // below delta, and then only for experts whose logit lies in
+  // (v[pos] - delta, v[pos-1] + delta). The selection boundary (ids output)
+  // flags on the gap alone; an evaluation-only boundary (1, k, m_list:
+  // metrics.py:159-180 count only where the TRUE experts rank) flags only when
+  // a true expert lies in that window — its counters cannot change otherwise.
+  const bool eval_only_ok = p.truth != nullptr && valid;
 #pragma unroll
   for (int b = 0; b < MOEP_MAX_BOUNDS; ++b) {
     if (b < p.n_bounds) {
@@ -128,7 +136,16 @@ __device__ __forceinline__ void row_epilogue(const Params& p, float* z, float su
 #pragma unroll
         for (int s = 1; s < kMaxSel; ++s)
           if (s == pos) { hi_v = tv[s - 1]; lo_v = tv[s]; }
-        flagged |= !(hi_v - lo_v >= delta);
+        if (!(hi_v - lo_v >= delta)) {
+          if ((p.ids && pos == p.m_sel) || !eval_only_ok) {
+            flagged = true;
+          } else {
+            for (int j = 0; j < p.k; ++j) {
+              const float zt = zrow[__ldg(p.truth + row * p.k + j) ^ zswz];
+              flagged |= !(zt <= lo_v - delta || zt >= hi_v + delta);
+            }
+          }
+        }
       }
     }
   }

@@ -190,6 +190,11 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       // ---------------------------------------------- TMA: x rows + W1 half-chunk
       if (elect_one()) {
         const uint64_t keep = policy_evict_last();
+#ifdef K1V4_X_NORMAL
+        const uint64_t xpol = policy_evict_normal();
+#else
+        const uint64_t xpol = keep;
+#endif
         uint32_t stage = 0, phase = 0;
         for (int item = pair; item < n_items; item += n_pairs) {
           const int tile = item / G, c0 = (item % G) * cpg;
@@ -212,7 +217,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
               if (ld_w) tma_load_2d_cg2(&tm_w1, &full[stage], smem + C::OFF_B + stage * C::B_BYTES, kb * BK, wrow, keep);
 #else
               if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
-              tma_load_2d_cg2(&tm_x, &full[stage], smem + C::OFF_A + stage * C::A_BYTES, kb * BK, xrow, keep);
+              tma_load_2d_cg2(&tm_x, &full[stage], smem + C::OFF_A + stage * C::A_BYTES, kb * BK, xrow, xpol);
               tma_load_2d_cg2(&tm_w1, &full[stage], smem + C::OFF_B + stage * C::B_BYTES, kb * BK, wrow, keep);
 #endif
               if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
