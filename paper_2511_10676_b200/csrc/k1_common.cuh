@@ -74,21 +74,10 @@ __device__ __forceinline__ bool test(uint64_t* bar, uint32_t parity) {
 // (predictor.py:347-351, core.py:42-48) and metrics.py:159-180.
 // zrow: this thread's smem staging row (>= EP floats) used for the dynamic
 // truth-expert lookups; hist: the calling warp's private [2][EP] histogram.
-template <int EP>
-__device__ __forceinline__ void row_epilogue(const Params& p, float* z, float sumsq, int64_t row, bool valid,
-                                             uint32_t lane, int* hist, RowCounters& rc, float* zrow,
-                                             uint32_t zswz) {
-  bool flagged = false;
-#pragma unroll
-  for (int e = 0; e < EP; ++e) {
-    if (e < p.E) {
-      z[e] += __ldg(p.b2 + e);
-      flagged |= !isfinite(z[e]);
-    } else {
-      z[e] = -INFINITY;
-    }
-    if (p.truth) zrow[e ^ zswz] = z[e];
-  }
+template <int EP, class ZGet>
+__device__ __forceinline__ void row_epilogue_core(const Params& p, ZGet zv, bool flagged, float sumsq, int64_t row,
+                                                  bool valid, uint32_t lane, int* hist, RowCounters& rc,
+                                                  const float* zrow, uint32_t zswz) {
   int P = p.m_sel;
 #pragma unroll
   for (int b = 0; b < MOEP_MAX_BOUNDS; ++b)
@@ -108,7 +97,7 @@ __device__ __forceinline__ void row_epilogue(const Params& p, float* z, float su
 #pragma unroll
         for (int e = 0; e < EP; ++e) {
           const bool tk = (taken[e >> 5] >> (e & 31)) & 1u;
-          if (!tk && z[e] > best) { best = z[e]; bi = e; }
+          if (!tk && zv(e) > best) { best = zv(e); bi = e; }
         }
 #pragma unroll
         for (int w = 0; w < (EP + 31) / 32; ++w)
@@ -159,7 +148,7 @@ __device__ __forceinline__ void row_epilogue(const Params& p, float* z, float su
       float* lrow = p.logits + row * p.E;
 #pragma unroll
       for (int e = 0; e < EP; ++e)
-        if (e < p.E) lrow[e] = z[e];
+        if (e < p.E) lrow[e] = zv(e);
     }
     if (p.ids && !flagged) {
       int* orow = p.ids + row * p.m_sel;
@@ -174,7 +163,7 @@ __device__ __forceinline__ void row_epilogue(const Params& p, float* z, float su
         int cnt = 0;
 #pragma unroll
         for (int e = 0; e < EP; ++e)
-          if (e < p.E && (key_gt(z[e], e, thv, thi) || e == thi)) orow[cnt++] = e;
+          if (e < p.E && (key_gt(zv(e), e, thv, thi) || e == thi)) orow[cnt++] = e;
       }
     }
   }
@@ -222,6 +211,37 @@ __device__ __forceinline__ void row_epilogue(const Params& p, float* z, float su
       }
     }
   }
+}
+
+
+// z[EP]: this token's raw GEMM2 accumulator (no b2) in registers.
+template <int EP>
+__device__ __forceinline__ void row_epilogue(const Params& p, float* z, float sumsq, int64_t row, bool valid,
+                                             uint32_t lane, int* hist, RowCounters& rc, float* zrow,
+                                             uint32_t zswz) {
+  bool flagged = false;
+#pragma unroll
+  for (int e = 0; e < EP; ++e) {
+    if (e < p.E) {
+      z[e] += __ldg(p.b2 + e);
+      flagged |= !isfinite(z[e]);
+    } else {
+      z[e] = -INFINITY;
+    }
+    if (p.truth) zrow[e ^ zswz] = z[e];
+  }
+  row_epilogue_core<EP>(p, [&](int e) { return z[e]; }, flagged, sumsq, row, valid, lane, hist, rc, zrow, zswz);
+}
+
+// Same epilogue over a token whose z + b2 is staged in shared memory (zrow,
+// written by the caller for every e < EP, -inf beyond E): only the top list
+// lives in registers, so the register footprint does not grow with E.
+template <int EP>
+__device__ __forceinline__ void row_epilogue_staged(const Params& p, bool flagged, float sumsq, int64_t row,
+                                                    bool valid, uint32_t lane, int* hist, RowCounters& rc,
+                                                    const float* zrow, uint32_t zswz) {
+  row_epilogue_core<EP>(p, [&](int e) { return zrow[e ^ zswz]; }, flagged, sumsq, row, valid, lane, hist, rc,
+                        zrow, zswz);
 }
 
 // Staging row for row_epilogue inside a 64 KB smem region (128 rows):

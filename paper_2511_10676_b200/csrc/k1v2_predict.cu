@@ -631,8 +631,9 @@ __global__ void __launch_bounds__(256) split_finish_kernel(const Params p) {
 }
 
 // Which pair kernel runs: v4 (k1v4_predict.cu: token epilogue on its own
-// warpgroup, A2 in TMEM) for unsplit launches with E <= 64, this file's v2
-// kernel otherwise (E = 128, hidden-split small-N launches).
+// warpgroup, A2 in TMEM) for unsplit launches with at least two 256-token
+// tiles per CTA pair, this file's v2 kernel otherwise (hidden-split small-N
+// launches, one-wave launches).
 // MOEP_K1_VARIANT=2 forces v2; =3 selects v3 (double-buffered accumulator,
 // 192-column chunks, E <= 64: removes the drain bubble but measured slower,
 // profiles/r01_k1_role_waits.md); =1 selects the 1-SM kernel in moep_predict_bf16.
@@ -648,8 +649,8 @@ static bool use_v3(int hidden, int n_experts) {
   return variant() == 3 && hidden % 64 == 0 && n_experts <= 64;  // EP = 128 spills in v3 (round 2)
 }
 // v4 (A2 in TMEM, 5-stage ring, token epilogue on its own warpgroup;
-// k1v4_predict.cu) for unsplit launches with E <= 64 (E = 128 spills there)
-static bool use_v4(int hidden, int n_experts) { return variant() == 4 && hidden % HC == 0 && n_experts <= 64; }
+// k1v4_predict.cu) for unsplit launches
+static bool use_v4(int hidden, int n_experts) { return variant() == 4 && hidden % HC == 0 && n_experts <= 128; }
 
 static int pair_chunks(int hidden, int n_experts) {
   return use_v3(hidden, n_experts) ? (hidden + 191) / 192 : hidden / HC;
@@ -748,7 +749,11 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
   if (use_v3(a->hidden, a->n_experts)) {
     const int rc = moep_predict_bf16_pair3(a, p.split, p.zpart, p.zpad, st);
     if (rc != MOEP_OK) return rc;
-  } else if (p.split == 1 && use_v4(a->hidden, a->n_experts)) {
+  } else if (p.split == 1 && use_v4(a->hidden, a->n_experts) &&
+             (a->n_tokens + 2 * BM - 1) / (2 * BM) >= 2 * (grid / 2)) {
+    // v4 hides each tile's token epilogue behind the next tile: with fewer
+    // than two tiles per CTA pair there is nothing to hide it behind, and v2's
+    // register-resident epilogue is the shorter path
     return moep_predict_bf16_pair4(a, st);
   } else {
     kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);

@@ -10,7 +10,8 @@
 // WG2 (warps 12-15) owns z: it reads the tile's z from TMEM (the MMA waits
 // only for that read, z_empty), takes the two ||h||^2 partials from WG0 / WG1
 // through a double-buffered shared-memory hand-off (sum_ready / sum_empty) and
-// runs the selection while the next tile's chunks stream. Chunk period
+// runs the selection while the next tile's chunks stream (over z staged in
+// shared memory, so its registers do not grow with E). Chunk period
 // 27.1 k -> 22.4 k cycles, no per-tile stall. 512 threads: setmaxnreg splits
 // the register file 72 (TMA / MMA warps) / 160 (chunk epilogue) / 120 (WG2).
 //
@@ -435,10 +436,27 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       wait(z_full, ti & 1);
       K1_TR(14, ti * 8 + 7, lane == 0 && q == 0);
       tc_fence_after();
-      float z[EP];
+      // z + b2 -> this row's shared-memory staging row (16 columns at a time:
+      // the register footprint stays flat in E)
+      uint32_t zswz;
+      float* zrow = k1c::zstage_row<EP>(smem + C::OFF_Z, row_in_tile, lane, zswz);
+      bool bad = false;
 #pragma unroll
-      for (int j = 0; j < EP; j += 16) tmem_ld16(tmem + lane_addr + C::ZCOL + j, z + j);
-      tmem_ld_wait();
+      for (int j = 0; j < EP; j += 16) {
+        float zc[16];
+        tmem_ld16(tmem + lane_addr + C::ZCOL + j, zc);
+        tmem_ld_wait();
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const int e = j + t;
+          float v = -INFINITY;
+          if (e < p.E) {
+            v = zc[t] + __ldg(p.b2 + e);
+            bad |= !isfinite(v);
+          }
+          zrow[e ^ zswz] = v;
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(z_empty, 0);
@@ -447,9 +465,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
                           s_sumsq[((ti & 1) * 2 + 1) * BM + row_in_tile];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sum_empty[ti & 1]);
-      uint32_t zswz;
-      float* zrow = k1c::zstage_row<EP>(smem + C::OFF_Z, row_in_tile, lane, zswz);
-      k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc, zrow, zswz);
+      k1c::row_epilogue_staged<EP>(p, bad, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc, zrow, zswz);
       K1_TR(15, ti * 8 + 7, lane == 0 && q == 0);
     }
     if (p.partials)
@@ -507,9 +523,9 @@ extern "C" int moep_k1v4_trace(long long* host) {
 }
 #endif
 
-// v4 pair kernel (no hidden split): hidden % 256 == 0, E <= 64.
+// v4 pair kernel (no hidden split): hidden % 256 == 0, E <= 128.
 extern "C" int moep_predict_bf16_pair4(const moep_predict_args* a, void* stream) {
-  if (a->n_experts > 64 || a->hidden % 256 != 0) return MOEP_EUNSUPPORTED;
+  if (a->n_experts > 128 || a->hidden % 256 != 0) return MOEP_EUNSUPPORTED;
   int EP = 16;
   while (EP < a->n_experts) EP *= 2;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -518,6 +534,6 @@ extern "C" int moep_predict_bf16_pair4(const moep_predict_args* a, void* stream)
     case 16: return a1 ? launch_v4<16, 1>(a, st) : launch_v4<16, 2>(a, st);
     case 32: return a1 ? launch_v4<32, 1>(a, st) : launch_v4<32, 2>(a, st);
     case 64: return a1 ? launch_v4<64, 1>(a, st) : launch_v4<64, 2>(a, st);
-    default: return MOEP_EUNSUPPORTED;  // E = 128: WG2's z[128] spills at its register share; v2 runs it
+    default: return a1 ? launch_v4<128, 1>(a, st) : launch_v4<128, 2>(a, st);
   }
 }
