@@ -196,6 +196,11 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
 #else
         const uint64_t xpol = keep;
 #endif
+#ifdef K1V4_W1_NORMAL
+        const uint64_t wpol = policy_evict_normal();
+#else
+        const uint64_t wpol = keep;
+#endif
         uint32_t stage = 0, phase = 0;
         for (int item = pair; item < n_items; item += n_pairs) {
           const int tile = item / G, c0 = (item % G) * cpg;
@@ -219,7 +224,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
 #else
               if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
               tma_load_2d_cg2(&tm_x, &full[stage], smem + C::OFF_A + stage * C::A_BYTES, kb * BK, xrow, xpol);
-              tma_load_2d_cg2(&tm_w1, &full[stage], smem + C::OFF_B + stage * C::B_BYTES, kb * BK, wrow, keep);
+              tma_load_2d_cg2(&tm_w1, &full[stage], smem + C::OFF_B + stage * C::B_BYTES, kb * BK, wrow, wpol);
 #endif
               if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
             }
@@ -436,10 +441,12 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       wait(z_full, ti & 1);
       K1_TR(14, ti * 8 + 7, lane == 0 && q == 0);
       tc_fence_after();
-      // z + b2 -> this row's shared-memory staging row (16 columns at a time:
-      // the register footprint stays flat in E)
       uint32_t zswz;
       float* zrow = k1c::zstage_row<EP>(smem + C::OFF_Z, row_in_tile, lane, zswz);
+      // z + b2 -> this row's shared-memory staging row, 16 columns at a time:
+      // the selection reads z from there, so WG2's registers do not grow with
+      // E (measured 1-3 % faster than register-resident z at E = 64, which
+      // spills at WG2's 120-register share)
       bool bad = false;
 #pragma unroll
       for (int j = 0; j < EP; j += 16) {

@@ -15,7 +15,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "tools", "_k1prof")
-FLAGS = {"XNORMAL": ["-DK1V4_X_NORMAL"], "TRACE": ["-DMOEP_K1_PROF"], "NOW1": ["-DMOEP_K1_EXP_NOW1"], "NOX": ["-DMOEP_K1_EXP_NOX"], "NOACT": ["-DMOEP_K1_PROF_NOACT"],
+FLAGS = {"W1NORMAL": ["-DK1V4_W1_NORMAL"], "XNORMAL": ["-DK1V4_X_NORMAL"], "TRACE": ["-DMOEP_K1_PROF"], "NOW1": ["-DMOEP_K1_EXP_NOW1"], "NOX": ["-DMOEP_K1_EXP_NOX"], "NOACT": ["-DMOEP_K1_PROF_NOACT"],
          "base": []}
 
 TIMER = r'''
