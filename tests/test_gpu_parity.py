@@ -113,7 +113,13 @@ CONFIGS = [
     # (arch, d, h, E, k, n)    C1/C2 DSV2L, C3 Qwen3, C4 Phi (inference), arch1
     ("arch2", 2048, 2048, 64, 6, 16384),
     ("arch2", 2048, 2048, 128, 8, 8192),
-    ("arch2", 2048, 2048, 128, 8, 20480),  # C3 Qwen3 with every CTA pair busy (unsplit v4 kernel, E = 128)
+    ("arch2", 2048, 2048, 128, 8, 20480),  # C3 Qwen3 with every CTA pair busy (unsplit, one wave: v2)
+    # >= 2 tiles of 256 per CTA pair (N >= 37,888 on 148 SMs): the v4 kernel
+    # (token epilogue on its own warpgroup, A2 in TMEM); ragged last tile
+    ("arch2", 2048, 2048, 64, 6, 40000),
+    ("arch2", 2048, 2048, 128, 8, 40000),
+    ("arch2", 4096, 2048, 16, 2, 40000),
+    ("arch1", 2048, 2048, 64, 6, 40000),
     ("arch2", 4096, 2048, 16, 2, 8192),
     ("arch1", 2048, 2048, 64, 6, 4096),
     ("arch2", 64, 128, 16, 2, 3000),     # ragged token count, small dims
