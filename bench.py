@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-prefetch", action="store_true")
     ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--no-synthgen", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -257,6 +258,9 @@ def main():
     prefetch = None
     if rank == 0 and not args.no_prefetch:
         prefetch = prefetch_arm(layers[0][1], layers[0][2], dev)
+    synth = None
+    if rank == 0 and not args.no_synthgen:
+        synth = synthgen_arm(dev)
 
     if rank == 0:
         line = {
@@ -274,7 +278,7 @@ def main():
                        "parallelism": f"token-sharded dp{world}"},
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": sustained, "unit": "TFLOP/s",
                          "frac": achieved_tflops / sustained, "peak_kind": f"{src} sustained bf16",
-                         "frac_of_burst": achieved_tflops / burst, "kernel": "moep k1 predict_kernel",
+                         "frac_of_burst": achieved_tflops / burst, "kernel": "moep k1v4::predict_pair_kernel (K1)",
                          "flop_per_token": FLOP_PER_TOKEN, "tokens_per_launch": args.tokens,
                          "k1_ms_per_launch": k1_ms, "k1_timing": "CUDA events around every K1 launch "
                                                                 "inside the timed region, mean",
@@ -295,6 +299,7 @@ def main():
             "e2e": e2e,
             "prefetch": prefetch,
             "train": train,
+            "synthgen": synth,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -346,6 +351,43 @@ def cpu_baseline(model, x, truth, n_sample=32768):
     return {"value": n_sample / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"{n_sample} tokens of layer 0: predict_logits + top_k_batch(6) + evaluate_predictions "
                       f"(oracle/oracle.py numpy fp64, OpenBLAS all threads), {dt:.2f} s"}
+
+
+def synthgen_arm(dev, n=262144, cpu_n=1024):
+    """the synthetic teacher (synthgen.generate_dataset_device,
+    K11 kernels) on one 262,144-sample DSV2L-shaped chunk, CUDA events, best of 3;
+    beside it the reference's per-sample loop (synthgen.py:170-174: one numpy
+    Generator(Philox(key)) per sample, then layer_norm + gate softmax + top-k) on
+    a bounded host sample."""
+    import torch
+    from paper_2511_10676_b200 import synthgen as sg
+    gate = np.random.default_rng(0).standard_normal((E, D)) / np.sqrt(D)
+    t = sg.TeacherSpec(sg.RouterSpec(D, E, K_ACT, gate), seed=0)
+    sg.generate_dataset_device(t, 4096, device=dev)
+    best = 1e30
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = sg.generate_dataset_device(t, n, device=dev)
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+        del out
+    t0 = time.perf_counter()
+    x = np.empty((cpu_n, D))
+    for i in range(cpu_n):
+        x[i] = np.random.Generator(np.random.Philox(key=i)).standard_normal(D)   # seed 0: key = (0 << 64) + i
+    post = (x - x.mean(-1, keepdims=True)) / np.sqrt(x.var(-1, keepdims=True) + 1e-5)
+    z = post @ gate.T
+    z = z - z.max(-1, keepdims=True)
+    sc = (np.exp(z) / np.exp(z).sum(-1, keepdims=True)).astype(np.float32)
+    np.sort(np.argsort(-sc.astype(np.float64), axis=1, kind="stable")[:, :K_ACT], axis=1)
+    cpu = cpu_n / (time.perf_counter() - t0)
+    return {"workload": "synthetic teacher, DSV2L shape (d=2048, E=64, top-6, identity + layer_norm), "
+                        "BASELINE-adjacent SURVEY 8(f) row 3",
+            "samples": n, "ms": best, "samples_per_s": n / (best / 1e3),
+            "cpu_reference": {"samples_per_s": cpu, "sample": f"{cpu_n} samples, the reference's per-sample "
+                              "numpy Philox loop + layer_norm + gate softmax + top-k", "cores": os.cpu_count()}}
 
 
 def prefetch_arm(dp, x, dev, batches=(1, 8, 32, 128, 256)):
