@@ -88,6 +88,167 @@ eval_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict__ t
   }
 }
 
+// Register-resident variants (E <= 32 * PL). One warp per token: lane l holds
+// z[l], z[l + 32], ...; the k true ids are one coalesced load; the stable rank
+// of each true expert is popc(ballot(key_gt)) over the row in registers (no
+// re-reads), its logit a shuffle. RPI tokens per warp iteration keep several
+// rows' loads in flight. Block = 32 warps, one block per SM: the partial
+// counter row layout [num_SMs][n_counters] is unchanged.
+constexpr int NTR = 1024;
+
+template <typename T, int PL>
+__device__ __forceinline__ T lane_pick(const T (&v)[PL], int q) {
+  T r = v[0];
+#pragma unroll
+  for (int i = 1; i < PL; ++i)
+    if (i == q) r = v[i];
+  return r;
+}
+
+template <typename T, int PL, int RPI>
+__global__ void __launch_bounds__(NTR)
+eval_reg_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict__ truth, int k,
+                int n_m, const int* __restrict__ m_list_dev, int* partials, int n_counters) {
+  extern __shared__ int sh[];  // [32 warps][2E] hist
+  __shared__ int scal[NTR / 32][2 + 2 * MOEP_MAX_BOUNDS];
+  __shared__ int mls[MOEP_MAX_BOUNDS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* hist = sh + warp * 2 * E;
+  for (int i = lane; i < 2 * E; i += 32) hist[i] = 0;
+  if (threadIdx.x < MOEP_MAX_BOUNDS) mls[threadIdx.x] = threadIdx.x < n_m ? m_list_dev[threadIdx.x] : 0;
+  __syncthreads();
+  int m_of[MOEP_MAX_BOUNDS];
+#pragma unroll
+  for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) m_of[mi] = mls[mi];
+  int cnt[2 + 2 * MOEP_MAX_BOUNDS];
+#pragma unroll
+  for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) cnt[i] = 0;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NTR / 32) + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (NTR / 32);
+  for (int64_t base = gw * RPI; base < n; base += nw * RPI) {
+    T zv[RPI][PL];
+    int tv[RPI];
+#pragma unroll
+    for (int r = 0; r < RPI; ++r) {  // every load of the RPI rows first
+      const int64_t row = base + r;
+      const bool ok = row < n;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const int e = q * 32 + lane;
+        zv[r][q] = (ok && e < E) ? z[row * E + e] : T(0);
+      }
+      tv[r] = (ok && lane < k) ? truth[row * k + lane] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < RPI; ++r) {
+      if (base + r >= n) break;  // warp-uniform
+      int my_rank = 0, any0 = 0;
+      int inside[MOEP_MAX_BOUNDS] = {0, 0, 0, 0};
+      for (int j = 0; j < k; ++j) {
+        const int t = __shfl_sync(0xffffffffu, tv[r], j);
+        const T zt = __shfl_sync(0xffffffffu, lane_pick<T, PL>(zv[r], t >> 5), t & 31);
+        int rk = 0;
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+          const int e = q * 32 + lane;
+          rk += __popc(__ballot_sync(0xffffffffu, e < E && key_gt(zv[r][q], e, zt, t)));
+        }
+        if (lane == j) my_rank = rk;
+        any0 |= rk == 0;
+#pragma unroll
+        for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) inside[mi] += rk < m_of[mi] ? 1 : 0;
+      }
+      // true ids of a token are distinct: lanes j < k update different bins
+      if (lane < k) {
+        hist[E + tv[r]] += 1;
+        if (my_rank < k) hist[tv[r]] += 1;
+      }
+      cnt[0] += 1;
+      cnt[1] += any0;
+#pragma unroll
+      for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
+        cnt[2 + mi] += inside[mi] == k ? 1 : 0;
+        cnt[2 + MOEP_MAX_BOUNDS + mi] += inside[mi];
+      }
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) scal[warp][i] = cnt[i];
+  }
+  __syncthreads();
+  int* out = partials + static_cast<int64_t>(blockIdx.x) * n_counters;
+  for (int t = threadIdx.x; t < n_counters; t += NTR) {
+    int v = 0;
+    if (t < 2 + 2 * n_m) {
+      const int src = t < 2 ? t : (t < 2 + n_m ? t : 2 + MOEP_MAX_BOUNDS + (t - 2 - n_m));
+      for (int w = 0; w < NTR / 32; ++w) v += scal[w][src];
+    } else {
+      const int e = t - 2 - 2 * n_m;
+      for (int w = 0; w < NTR / 32; ++w) v += sh[w * 2 * E + e];
+    }
+    out[t] = v;
+  }
+}
+
+// top-m ids (m <= 16) ascending: m rounds of warp argmax under the reference
+// key (value, then lower index), then a ballot prefix over expert order.
+template <typename T, int PL, int RPI>
+__global__ void __launch_bounds__(256)
+topk_reg_kernel(const T* __restrict__ z, int64_t n, int E, int m, int* __restrict__ ids) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * 8;
+  for (int64_t base = gw * RPI; base < n; base += nw * RPI) {
+    T zv[RPI][PL];
+#pragma unroll
+    for (int r = 0; r < RPI; ++r) {
+      const int64_t row = base + r;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const int e = q * 32 + lane;
+        zv[r][q] = (row < n && e < E) ? z[row * E + e] : T(0);
+      }
+    }
+    // the RPI rows' argmax rounds interleaved (independent chains)
+    uint32_t taken[RPI];
+#pragma unroll
+    for (int r = 0; r < RPI; ++r) taken[r] = 0;
+    for (int s = 0; s < m; ++s) {
+#pragma unroll
+      for (int r = 0; r < RPI; ++r) {
+        T best = T(0);
+        int bi = -1;
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+          const int e = q * 32 + lane;
+          if (e < E && !((taken[r] >> q) & 1u) && (bi < 0 || key_gt(zv[r][q], e, best, bi))) { best = zv[r][q]; bi = e; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const T ov = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (oi >= 0 && (bi < 0 || key_gt(ov, oi, best, bi))) { best = ov; bi = oi; }
+        }
+        if ((bi & 31) == lane) taken[r] |= 1u << (bi >> 5);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPI; ++r) {
+      const int64_t row = base + r;
+      if (row >= n) break;  // warp-uniform
+      int written = 0;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const bool sel = (taken[r] >> q) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+        if (sel) ids[row * m + written + __popc(bal & ((1u << lane) - 1u))] = q * 32 + lane;
+        written += __popc(bal);
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(NT)
 topk_kernel(const T* __restrict__ z, int64_t n, int E, int m, int* __restrict__ ids) {
@@ -258,6 +419,29 @@ int moep_eval_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, co
   if (smem > 200 * 1024) return MOEP_EUNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = moep_num_sms();
+  if (E <= 256) {
+    const size_t smem_r = sizeof(int) * 2 * E * (NTR / 32);
+#define MOEP_K7E(T, PL)                                                                                     \
+  do {                                                                                                      \
+    auto kern = eval_reg_kernel<T, PL, 2>;                                                                  \
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r) != cudaSuccess) \
+      return MOEP_ELAUNCH;                                                                                  \
+    kern<<<grid, NTR, smem_r, st>>>(static_cast<const T*>(logits), n, E, truth, k, n_m, m_list, partials, ncnt); \
+  } while (0)
+#define MOEP_K7E_T(T)                        \
+  do {                                       \
+    if (E <= 32) MOEP_K7E(T, 1);             \
+    else if (E <= 64) MOEP_K7E(T, 2);        \
+    else if (E <= 128) MOEP_K7E(T, 4);       \
+    else MOEP_K7E(T, 8);                     \
+  } while (0)
+    if (dtype == MOEP_F64) MOEP_K7E_T(double);
+    else if (dtype == MOEP_F32) MOEP_K7E_T(float);
+    else return MOEP_EARG;
+#undef MOEP_K7E_T
+#undef MOEP_K7E
+    return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+  }
   if (dtype == MOEP_F64) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(eval_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     eval_kernel<double><<<grid, NT, smem, st>>>(static_cast<const double*>(logits), n, E, truth, k, n_m, m_list, partials, ncnt);
@@ -277,6 +461,24 @@ int moep_topk_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, in
   if (m < 1 || m > E) return MOEP_EARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = moep_num_sms() * 4;
+  if (E <= 256 && m <= 16) {
+    const int64_t want = (n + 31) / 32;  // 8 warps x 4 rows per block iteration
+    const int g2 = static_cast<int>(want < 8 * moep_num_sms() ? want : 8 * moep_num_sms());
+#define MOEP_K7T(T, PL) topk_reg_kernel<T, PL, 4><<<g2, 256, 0, st>>>(static_cast<const T*>(logits), n, E, m, ids)
+#define MOEP_K7T_T(T)                  \
+  do {                                 \
+    if (E <= 32) MOEP_K7T(T, 1);       \
+    else if (E <= 64) MOEP_K7T(T, 2);  \
+    else if (E <= 128) MOEP_K7T(T, 4); \
+    else MOEP_K7T(T, 8);               \
+  } while (0)
+    if (dtype == MOEP_F64) MOEP_K7T_T(double);
+    else if (dtype == MOEP_F32) MOEP_K7T_T(float);
+    else return MOEP_EARG;
+#undef MOEP_K7T_T
+#undef MOEP_K7T
+    return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+  }
   if (dtype == MOEP_F64)
     topk_kernel<double><<<grid, NT, 0, st>>>(static_cast<const double*>(logits), n, E, m, ids);
   else if (dtype == MOEP_F32)

@@ -58,6 +58,68 @@ labels_kernel(const T* __restrict__ s, int64_t n, int E, int k, int top_cut, int
   }
 }
 
+// Register-resident K3 (E <= 32 * EPL): LPR lanes per token, the row's scores
+// in registers, every comparison against the other experts by width-LPR
+// shuffles (no re-reads); same outputs as labels_kernel.
+template <typename T, int LPR, int EPL>
+__global__ void __launch_bounds__(NT)
+labels_reg_kernel(const T* __restrict__ s, int64_t n, int E, int k, int top_cut, int* __restrict__ rank_of,
+                  uint8_t* __restrict__ mask, int* __restrict__ pairs) {
+  constexpr int RPW = 32 / LPR;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / LPR, li = lane % LPR;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  for (int64_t base = gw * RPW; base < n; base += nw * RPW) {  // warp-uniform
+    const int64_t row = base + sub;
+    T sv[EPL];
+    int rk[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      const int e = li + i * LPR;
+      sv[i] = (row < n && e < E) ? s[row * E + e] : T(0);
+      rk[i] = 0;
+    }
+#pragma unroll
+    for (int jb = 0; jb < EPL; ++jb) {
+      for (int jl = 0; jl < LPR; ++jl) {
+        const int j = jb * LPR + jl;
+        if (j >= E) break;  // uniform
+        const T sj = __shfl_sync(0xffffffffu, sv[jb], jl, LPR);
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) rk[i] += key_gt(sj, j, sv[i], li + i * LPR) ? 1 : 0;
+      }
+    }
+    // strict pairs among the true top-T (losses.py:202-207)
+    int np = 0;
+#pragma unroll
+    for (int jb = 0; jb < EPL; ++jb) {
+      for (int jl = 0; jl < LPR; ++jl) {
+        const int j = jb * LPR + jl;
+        if (j >= E) break;
+        const T sj = __shfl_sync(0xffffffffu, sv[jb], jl, LPR);
+        const int rj = __shfl_sync(0xffffffffu, rk[jb], jl, LPR);
+#pragma unroll
+        for (int i = 0; i < EPL; ++i)
+          np += (li + i * LPR < E && rk[i] < top_cut && rj < top_cut && sv[i] > sj) ? 1 : 0;
+      }
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+    if (row < n) {
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const int e = li + i * LPR;
+        if (e < E) {
+          rank_of[row * E + e] = rk[i] + 1;
+          mask[row * E + e] = rk[i] < k ? 1 : 0;
+        }
+      }
+      if (li == 0 && pairs) pairs[row] = np;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K4
 struct LossParams {
   int family;  // 0 mse, 1 wbce, 2 focal, 3 ranking
@@ -715,6 +777,26 @@ int moep_labels(const void* scores, int32_t dtype, int64_t n, int32_t E, int32_t
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = moep_num_sms() * 4;
   const int top_cut = E < 10 ? E : 10;  // TOP_TIER_SIZE (losses.py:27)
+  if (E <= 256) {
+#define MOEP_K3(T, LPR, EPL)                                                                                \
+  labels_reg_kernel<T, LPR, EPL><<<grid, NT, 0, st>>>(static_cast<const T*>(scores), n, E, k, top_cut, rank_of, \
+                                                      topk_mask, pair_count)
+#define MOEP_K3_T(T)                        \
+  do {                                      \
+    if (E <= 8) MOEP_K3(T, 8, 1);           \
+    else if (E <= 16) MOEP_K3(T, 16, 1);    \
+    else if (E <= 32) MOEP_K3(T, 32, 1);    \
+    else if (E <= 64) MOEP_K3(T, 32, 2);    \
+    else if (E <= 128) MOEP_K3(T, 32, 4);   \
+    else MOEP_K3(T, 32, 8);                 \
+  } while (0)
+    if (dtype == MOEP_F64) MOEP_K3_T(double);
+    else if (dtype == MOEP_F32) MOEP_K3_T(float);
+    else return MOEP_EARG;
+#undef MOEP_K3_T
+#undef MOEP_K3
+    return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+  }
   if (dtype == MOEP_F64)
     labels_kernel<double><<<grid, NT, 0, st>>>(static_cast<const double*>(scores), n, E, k, top_cut, rank_of,
                                                  topk_mask, pair_count);
