@@ -88,12 +88,12 @@ eval_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict__ t
   }
 }
 
-// Register-resident variants (E <= 32 * PL). One warp per token: lane l holds
-// z[l], z[l + 32], ...; the k true ids are one coalesced load; the stable rank
-// of each true expert is popc(ballot(key_gt)) over the row in registers (no
-// re-reads), its logit a shuffle. RPI tokens per warp iteration keep several
-// rows' loads in flight. Block = 32 warps, one block per SM: the partial
-// counter row layout [num_SMs][n_counters] is unchanged.
+// Register-resident variants. The row of logits sits in registers (16 or 32
+// lanes per token); the k true ids are one coalesced load; the stable rank of
+// each true expert is popc(ballot(key_gt)) over the row (no re-reads), its
+// logit a shuffle. Several tokens per warp iteration keep their loads in
+// flight together. Block = 32 warps, one block per SM: the partial counter
+// row layout [num_SMs][n_counters] is unchanged.
 constexpr int NTR = 1024;
 
 template <typename T, int PL>
@@ -105,14 +105,20 @@ __device__ __forceinline__ T lane_pick(const T (&v)[PL], int q) {
   return r;
 }
 
-template <typename T, int PL, int RPI>
+template <typename T, int LPR, int EPL, int RPI>
 __global__ void __launch_bounds__(NTR)
 eval_reg_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict__ truth, int k,
                 int n_m, const int* __restrict__ m_list_dev, int* partials, int n_counters) {
+  // LPR lanes per token (k <= LPR), expert e = i * LPR + lane_in_row held in
+  // slot i; 32 / LPR tokens side by side in a warp, RPI such groups per
+  // iteration.
+  constexpr int RPW = 32 / LPR;
   extern __shared__ int sh[];  // [32 warps][2E] hist
   __shared__ int scal[NTR / 32][2 + 2 * MOEP_MAX_BOUNDS];
   __shared__ int mls[MOEP_MAX_BOUNDS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / LPR, li = lane % LPR;
+  const uint32_t submask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
   int* hist = sh + warp * 2 * E;
   for (int i = lane; i < 2 * E; i += 32) hist[i] = 0;
   if (threadIdx.x < MOEP_MAX_BOUNDS) mls[threadIdx.x] = threadIdx.x < n_m ? m_list_dev[threadIdx.x] : 0;
@@ -125,52 +131,67 @@ eval_reg_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict
   for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) cnt[i] = 0;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NTR / 32) + warp;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * (NTR / 32);
-  for (int64_t base = gw * RPI; base < n; base += nw * RPI) {
-    T zv[RPI][PL];
+  for (int64_t base = gw * RPI * RPW; base < n; base += nw * RPI * RPW) {
+    T zv[RPI][EPL];
     int tv[RPI];
 #pragma unroll
-    for (int r = 0; r < RPI; ++r) {  // every load of the RPI rows first
-      const int64_t row = base + r;
+    for (int r = 0; r < RPI; ++r) {  // every load of the group's rows first
+      const int64_t row = base + r * RPW + sub;
       const bool ok = row < n;
 #pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        const int e = q * 32 + lane;
-        zv[r][q] = (ok && e < E) ? z[row * E + e] : T(0);
+      for (int i = 0; i < EPL; ++i) {
+        const int e = i * LPR + li;
+        zv[r][i] = (ok && e < E) ? z[row * E + e] : T(0);
       }
-      tv[r] = (ok && lane < k) ? truth[row * k + lane] : 0;
+      tv[r] = (ok && li < k) ? truth[row * k + li] : 0;
     }
 #pragma unroll
     for (int r = 0; r < RPI; ++r) {
-      if (base + r >= n) break;  // warp-uniform
+      if (base + r * RPW >= n) break;  // warp-uniform
+      const bool ok = base + r * RPW + sub < n;
       int my_rank = 0, any0 = 0;
       int inside[MOEP_MAX_BOUNDS] = {0, 0, 0, 0};
       for (int j = 0; j < k; ++j) {
-        const int t = __shfl_sync(0xffffffffu, tv[r], j);
-        const T zt = __shfl_sync(0xffffffffu, lane_pick<T, PL>(zv[r], t >> 5), t & 31);
+        const int t = __shfl_sync(0xffffffffu, tv[r], j, LPR);
+        const T zt = __shfl_sync(0xffffffffu, lane_pick<T, EPL>(zv[r], t / LPR), t % LPR, LPR);
         int rk = 0;
 #pragma unroll
-        for (int q = 0; q < PL; ++q) {
-          const int e = q * 32 + lane;
-          rk += __popc(__ballot_sync(0xffffffffu, e < E && key_gt(zv[r][q], e, zt, t)));
+        for (int i = 0; i < EPL; ++i) {
+          const int e = i * LPR + li;
+          rk += __popc(__ballot_sync(0xffffffffu, e < E && key_gt(zv[r][i], e, zt, t)) & submask);
         }
-        if (lane == j) my_rank = rk;
+        if (li == j) my_rank = rk;
         any0 |= rk == 0;
 #pragma unroll
         for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) inside[mi] += rk < m_of[mi] ? 1 : 0;
       }
-      // true ids of a token are distinct: lanes j < k update different bins
-      if (lane < k) {
-        hist[E + tv[r]] += 1;
-        if (my_rank < k) hist[tv[r]] += 1;
+      // true ids of a token are distinct: lanes j < k of a token update
+      // different bins; the tokens of a warp use their own hist copies in turn
+      for (int g = 0; g < RPW; ++g) {
+        if (sub == g && ok && li < k) {
+          hist[E + tv[r]] += 1;
+          if (my_rank < k) hist[tv[r]] += 1;
+        }
+        __syncwarp();
       }
-      cnt[0] += 1;
-      cnt[1] += any0;
+      if (ok && li == 0) {
+        cnt[0] += 1;
+        cnt[1] += any0;
 #pragma unroll
-      for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
-        cnt[2 + mi] += inside[mi] == k ? 1 : 0;
-        cnt[2 + MOEP_MAX_BOUNDS + mi] += inside[mi];
+        for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
+          cnt[2 + mi] += inside[mi] == k ? 1 : 0;
+          cnt[2 + MOEP_MAX_BOUNDS + mi] += inside[mi];
+        }
       }
     }
+  }
+  // the row-group leaders (li == 0) hold the counts: sum them over the warp
+#pragma unroll
+  for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) {
+    int v = cnt[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    cnt[i] = v;
   }
   if (lane == 0) {
 #pragma unroll
@@ -421,19 +442,22 @@ int moep_eval_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, co
   const int grid = moep_num_sms();
   if (E <= 256) {
     const size_t smem_r = sizeof(int) * 2 * E * (NTR / 32);
-#define MOEP_K7E(T, PL)                                                                                     \
+#define MOEP_K7E(T, LPR, EPL)                                                                               \
   do {                                                                                                      \
-    auto kern = eval_reg_kernel<T, PL, 2>;                                                                  \
+    auto kern = eval_reg_kernel<T, LPR, EPL, 2>;                                                            \
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r) != cudaSuccess) \
       return MOEP_ELAUNCH;                                                                                  \
     kern<<<grid, NTR, smem_r, st>>>(static_cast<const T*>(logits), n, E, truth, k, n_m, m_list, partials, ncnt); \
   } while (0)
-#define MOEP_K7E_T(T)                        \
-  do {                                       \
-    if (E <= 32) MOEP_K7E(T, 1);             \
-    else if (E <= 64) MOEP_K7E(T, 2);        \
-    else if (E <= 128) MOEP_K7E(T, 4);       \
-    else MOEP_K7E(T, 8);                     \
+#define MOEP_K7E_T(T)                                                \
+  do {                                                               \
+    if (E <= 16 && k <= 16) MOEP_K7E(T, 16, 1);                      \
+    else if (E <= 32 && k <= 16) MOEP_K7E(T, 16, 2);                 \
+    else if (E <= 64 && k <= 16) MOEP_K7E(T, 16, 4);                 \
+    else if (E <= 32) MOEP_K7E(T, 32, 1);                            \
+    else if (E <= 64) MOEP_K7E(T, 32, 2);                            \
+    else if (E <= 128) MOEP_K7E(T, 32, 4);                           \
+    else MOEP_K7E(T, 32, 8);                                         \
   } while (0)
     if (dtype == MOEP_F64) MOEP_K7E_T(double);
     else if (dtype == MOEP_F32) MOEP_K7E_T(float);
