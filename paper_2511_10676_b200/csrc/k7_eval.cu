@@ -212,26 +212,30 @@ eval_reg_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict
   }
 }
 
-// top-m ids (m <= 16) ascending: m rounds of warp argmax under the reference
-// key (value, then lower index), then a ballot prefix over expert order.
-template <typename T, int PL, int RPI>
+// top-m ids (m <= 16) ascending: m rounds of argmax over the token's LPR
+// lanes under the reference key (value, then lower index), then a ballot
+// prefix over expert order. 32 / LPR tokens side by side per warp, RPI groups
+// interleaved round by round (independent chains).
+template <typename T, int LPR, int EPL, int RPI>
 __global__ void __launch_bounds__(256)
 topk_reg_kernel(const T* __restrict__ z, int64_t n, int E, int m, int* __restrict__ ids) {
+  constexpr int RPW = 32 / LPR;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / LPR, li = lane % LPR;
+  const uint32_t submask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * 8 + warp;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * 8;
-  for (int64_t base = gw * RPI; base < n; base += nw * RPI) {
-    T zv[RPI][PL];
+  for (int64_t base = gw * RPI * RPW; base < n; base += nw * RPI * RPW) {
+    T zv[RPI][EPL];
 #pragma unroll
     for (int r = 0; r < RPI; ++r) {
-      const int64_t row = base + r;
+      const int64_t row = base + r * RPW + sub;
 #pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        const int e = q * 32 + lane;
-        zv[r][q] = (row < n && e < E) ? z[row * E + e] : T(0);
+      for (int i = 0; i < EPL; ++i) {
+        const int e = i * LPR + li;
+        zv[r][i] = (row < n && e < E) ? z[row * E + e] : T(0);
       }
     }
-    // the RPI rows' argmax rounds interleaved (independent chains)
     uint32_t taken[RPI];
 #pragma unroll
     for (int r = 0; r < RPI; ++r) taken[r] = 0;
@@ -241,29 +245,28 @@ topk_reg_kernel(const T* __restrict__ z, int64_t n, int E, int m, int* __restric
         T best = T(0);
         int bi = -1;
 #pragma unroll
-        for (int q = 0; q < PL; ++q) {
-          const int e = q * 32 + lane;
-          if (e < E && !((taken[r] >> q) & 1u) && (bi < 0 || key_gt(zv[r][q], e, best, bi))) { best = zv[r][q]; bi = e; }
+        for (int i = 0; i < EPL; ++i) {
+          const int e = i * LPR + li;
+          if (e < E && !((taken[r] >> i) & 1u) && (bi < 0 || key_gt(zv[r][i], e, best, bi))) { best = zv[r][i]; bi = e; }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = LPR / 2; o > 0; o >>= 1) {
           const T ov = __shfl_xor_sync(0xffffffffu, best, o);
           const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
           if (oi >= 0 && (bi < 0 || key_gt(ov, oi, best, bi))) { best = ov; bi = oi; }
         }
-        if ((bi & 31) == lane) taken[r] |= 1u << (bi >> 5);
+        if (bi >= 0 && bi % LPR == li) taken[r] |= 1u << (bi / LPR);
       }
     }
 #pragma unroll
     for (int r = 0; r < RPI; ++r) {
-      const int64_t row = base + r;
-      if (row >= n) break;  // warp-uniform
+      const int64_t row = base + r * RPW + sub;
       int written = 0;
 #pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        const bool sel = (taken[r] >> q) & 1u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, sel);
-        if (sel) ids[row * m + written + __popc(bal & ((1u << lane) - 1u))] = q * 32 + lane;
+      for (int i = 0; i < EPL; ++i) {
+        const bool sel = (taken[r] >> i) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, sel) & submask;
+        if (sel && row < n) ids[row * m + written + __popc(bal & ((1u << lane) - 1u))] = i * LPR + li;
         written += __popc(bal);
       }
     }
@@ -486,15 +489,16 @@ int moep_topk_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = moep_num_sms() * 4;
   if (E <= 256 && m <= 16) {
-    const int64_t want = (n + 31) / 32;  // 8 warps x 4 rows per block iteration
+    const int64_t want = (n + 63) / 64;  // 8 warps x 4 groups x 2 rows per block iteration
     const int g2 = static_cast<int>(want < 8 * moep_num_sms() ? want : 8 * moep_num_sms());
-#define MOEP_K7T(T, PL) topk_reg_kernel<T, PL, 4><<<g2, 256, 0, st>>>(static_cast<const T*>(logits), n, E, m, ids)
-#define MOEP_K7T_T(T)                  \
-  do {                                 \
-    if (E <= 32) MOEP_K7T(T, 1);       \
-    else if (E <= 64) MOEP_K7T(T, 2);  \
-    else if (E <= 128) MOEP_K7T(T, 4); \
-    else MOEP_K7T(T, 8);               \
+#define MOEP_K7T(T, LPR, EPL) topk_reg_kernel<T, LPR, EPL, 4><<<g2, 256, 0, st>>>(static_cast<const T*>(logits), n, E, m, ids)
+#define MOEP_K7T_T(T)                        \
+  do {                                       \
+    if (E <= 16) MOEP_K7T(T, 16, 1);         \
+    else if (E <= 32) MOEP_K7T(T, 16, 2);    \
+    else if (E <= 64) MOEP_K7T(T, 16, 4);    \
+    else if (E <= 128) MOEP_K7T(T, 32, 4);   \
+    else MOEP_K7T(T, 32, 8);                 \
   } while (0)
     if (dtype == MOEP_F64) MOEP_K7T_T(double);
     else if (dtype == MOEP_F32) MOEP_K7T_T(float);
