@@ -137,6 +137,15 @@ __device__ __forceinline__ double sigm(double u) {
   const double eu = exp(u);
   return eu / (1.0 + eu);
 }
+// fp32 forms for fp32 logits (the tensor-core training modes; their loss is
+// checked to rel 1e-3 against the fp64 oracle step): full-precision expf /
+// log1pf, ~10x cheaper than the fp64 library calls
+__device__ __forceinline__ float softplus(float v) { return v > 0.f ? v + log1pf(expf(-v)) : log1pf(expf(v)); }
+__device__ __forceinline__ float sigm(float u) {
+  if (u >= 0.f) return 1.f / (1.f + expf(-u));
+  const float eu = expf(u);
+  return eu / (1.f + eu);
+}
 
 // Generic fallback (E > 512): one warp per token.
 // partials per CTA: [0] loss (bce/mse/focal part), [1] hinge total (unnormalised), [2] n_pairs
@@ -262,10 +271,11 @@ loss_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restr
   const int sub = lane / LPR, li = lane % LPR;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  using M = T;  // per-element math in the logits' precision; sums in fp64
   double l_main = 0.0, l_hinge = 0.0, n_pairs = 0.0;
   for (int64_t base = gw * RPW; base < n; base += nw * RPW) {  // warp-uniform
     const int64_t row = base + sub;
-    double zv[EPL], sv[EPL];
+    M zv[EPL], sv[EPL];
     int rk[EPL];
     bool pos[EPL], ev[EPL];
 #pragma unroll
@@ -273,42 +283,45 @@ loss_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restr
       const int e = li + i * LPR;
       ev[i] = row < n && e < E;
       const int64_t o = row * E + e;
-      zv[i] = ev[i] ? static_cast<double>(z[o]) : 0.0;
-      sv[i] = ev[i] ? static_cast<double>(s[o]) : 0.0;
+      zv[i] = ev[i] ? z[o] : M(0);
+      sv[i] = ev[i] ? s[o] : M(0);
       rk[i] = ev[i] ? rank_of[o] : 0x7fffffff;
       pos[i] = ev[i] && mask[o] != 0;
     }
     if (p.family == 0) {
       // MSE on softmax probabilities (losses.py:99-110, chain rule :250-255)
-      double mx = -INFINITY;
+      M mx = -INFINITY;
 #pragma unroll
       for (int i = 0; i < EPL; ++i)
-        if (ev[i]) mx = fmax(mx, zv[i]);
+        if (ev[i]) mx = mx > zv[i] ? mx : zv[i];
 #pragma unroll
-      for (int o = LPR / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      double ex[EPL], se = 0.0;
+      for (int o = LPR / 2; o > 0; o >>= 1) {
+        const M om = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = mx > om ? mx : om;
+      }
+      M ex[EPL], se = M(0);
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
-        ex[i] = ev[i] ? exp(zv[i] - mx) : 0.0;
+        ex[i] = ev[i] ? exp(zv[i] - mx) : M(0);
         se += ex[i];
       }
 #pragma unroll
       for (int o = LPR / 2; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-      double inner = 0.0;
+      M inner = M(0);
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
         if (!ev[i]) continue;
         ex[i] /= se;  // probability
-        const double diff = sv[i] - ex[i];
-        l_main += diff * diff * p.inv_n;
-        inner += (-2.0 * diff * p.inv_n) * ex[i];
+        const M diff = sv[i] - ex[i];
+        l_main += static_cast<double>(diff) * diff * p.inv_n;
+        inner += (M(-2) * diff * M(p.inv_n)) * ex[i];
       }
 #pragma unroll
       for (int o = LPR / 2; o > 0; o >>= 1) inner += __shfl_xor_sync(0xffffffffu, inner, o);
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
         if (!ev[i]) continue;
-        const double dp = -2.0 * (sv[i] - ex[i]) * p.inv_n;
+        const M dp = M(-2) * (sv[i] - ex[i]) * M(p.inv_n);
         dz[row * E + li + i * LPR] = static_cast<T>(ex[i] * (dp - inner));
       }
       continue;
@@ -316,27 +329,27 @@ loss_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restr
 #pragma unroll
     for (int i = 0; i < EPL; ++i) {
       if (!ev[i]) continue;
-      const double zi = zv[i];
-      double g = 0.0;
+      const M zi = zv[i];
+      M g = M(0);
       if (p.family == 2) {
         // focal (losses.py:156-179)
-        const double log_pt = pos[i] ? -softplus(-zi) : -softplus(zi);
-        const double pt = exp(log_pt);
-        const double at = pos[i] ? p.alpha : 1.0 - p.alpha;
-        const double om = 1.0 - pt;
-        const double focus = pow(om, p.gamma);
-        l_main += -at * focus * log_pt * p.inv_ne;
-        const double sgn = pos[i] ? 1.0 : -1.0;
-        g = at * sgn * (p.gamma * pt * focus * log_pt - pow(om, p.gamma + 1.0)) * p.inv_ne;
+        const M log_pt = pos[i] ? -softplus(-zi) : -softplus(zi);
+        const M pt = exp(log_pt);
+        const M at = M(pos[i] ? p.alpha : 1.0 - p.alpha);
+        const M om = M(1) - pt;
+        const M focus = pow(om, M(p.gamma));
+        l_main += -static_cast<double>(at) * focus * log_pt * p.inv_ne;
+        const M sgn = pos[i] ? M(1) : M(-1);
+        g = at * sgn * (M(p.gamma) * pt * focus * log_pt - pow(om, M(p.gamma + 1.0))) * M(p.inv_ne);
       } else if (p.family != 4) {
         // tier weights (losses.py:113-121); three tiers only for the ranking family
         const int r = rk[i];
         double w = p.rest_w;
         if (p.family == 3 && r > p.top_cut && r <= p.mid_cut) w = p.mid_w;
         if (r <= p.top_cut) w = p.top_w;
-        const double lt = pos[i] ? -softplus(-zi) : -softplus(zi);
-        l_main += -w * lt * p.inv_ne;
-        g = w * (sigm(zi) - (pos[i] ? 1.0 : 0.0)) * p.inv_ne;
+        const M lt = pos[i] ? -softplus(-zi) : -softplus(zi);
+        l_main += -w * static_cast<double>(lt) * p.inv_ne;
+        g = M(w) * (sigm(zi) - (pos[i] ? M(1) : M(0))) * M(p.inv_ne);
       }
       dz[row * E + li + i * LPR] = static_cast<T>(g);  // family 4 (hinge only): 0
     }
@@ -351,8 +364,8 @@ loss_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restr
         for (int jl = 0; jl < LPR; ++jl) {
           const int j = jb * LPR + jl;
           if (j >= E) break;
-          const double sj = __shfl_sync(0xffffffffu, sv[jb], jl, LPR);
-          const double zj = __shfl_sync(0xffffffffu, zv[jb], jl, LPR);
+          const M sj = __shfl_sync(0xffffffffu, sv[jb], jl, LPR);
+          const M zj = __shfl_sync(0xffffffffu, zv[jb], jl, LPR);
           const int rj = __shfl_sync(0xffffffffu, rk[jb], jl, LPR);
           const bool jtop = rj <= p.top_cut;  // (no divergent exit before the next shuffles)
 #pragma unroll
@@ -360,10 +373,10 @@ loss_kernel(const T* __restrict__ z, const T* __restrict__ s, const int* __restr
             if (!jtop || !ev[i] || rk[i] > p.top_cut || li + i * LPR == j) continue;
             if (sv[i] > sj) {  // e outranks j in truth: pair (e, j)
               n_pairs += 1.0;
-              const double gap = p.margin - (zv[i] - zj);
+              const M gap = M(p.margin) - (zv[i] - zj);
               if (gap > 0) { l_hinge += gap; gh[i] -= 1.0; }
             } else if (sj > sv[i]) {  // pair (j, e)
-              const double gap = p.margin - (zj - zv[i]);
+              const M gap = M(p.margin) - (zj - zv[i]);
               if (gap > 0) gh[i] += 1.0;
             }
           }
