@@ -8,9 +8,10 @@
 //     staging its own 128 x-rows and half of the W1 chunk (128 rows) -> per-SM
 //     shared-memory traffic per MAC is half of the 1-SM 128x128 tile, and x is
 //     re-streamed h/256 instead of h/128 times;
-//   * GEMM1 accumulates a 256-column chunk in TMEM (single buffer); the epilogue
-//     drains it into registers at once (setmaxnreg gives the epilogue 224 regs)
-//     so the next chunk's MMAs start after a short drain;
+//   * GEMM1 accumulates a 256-column chunk in TMEM (single buffer); each
+//     epilogue thread drains its 128 columns into registers at once (384
+//     threads, up to 168 registers each) so the next chunk's MMAs start after
+//     a short drain;
 //   * bias + activation + bf16 hi/lo split go to a 64 KB smem A operand, fed to
 //     GEMM2 (M=256, N=E) in two K-halves so one buffer suffices;
 //   * the per-token selection / margin flag / evaluation epilogue is shared
@@ -19,6 +20,9 @@
 // 2 TMA W2, 3 TMEM alloc, 4-11 epilogue (WG0 = columns 0-127 of the chunk and
 // the token epilogue, WG1 = columns 128-255).
 // Requires hidden % 256 == 0 and E <= 128 (else the 1-SM kernel is used).
+// Large launches (>= 2 tiles per CTA pair) run the v4 kernel instead
+// (k1v4_predict.cu: token epilogue on its own warpgroup, A2 in TMEM); this
+// kernel serves the hidden-split and one-wave launches.
 #include <cstdio>
 #include <cuda.h>
 #include "sm100.cuh"
