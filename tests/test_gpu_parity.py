@@ -211,6 +211,34 @@ def test_ties_go_to_fp64_and_lower_index(pb, O):
         assert np.array_equal(pb.predict_topk_batch(m, x, mm), O.top_k_batch(zref, mm))
 
 
+def test_eval_margin_flags_only_true_expert_ties(pb, O):
+    """Evaluation-only boundaries (no ids output): an exact logit tie between
+    experts 2 and 5 can only change the counters when a TRUE expert sits in the
+    tie window. With truth sets that avoid both, no token is flagged yet every
+    counter equals the oracle's; with truth sets that contain them, the tied
+    tokens are flagged, recomputed in fp64, and the counters still match."""
+    rng = np.random.default_rng(17)
+    e, k = 16, 2
+    m = bf16_model(pb, O, "arch2", 256, 256, e, seed=4)
+    m.w2[5] = m.w2[2]
+    x = O.round_bf16(rng.standard_normal((4096, 256)))
+    zref = O.predict_logits(oracle_params(m), x)
+    dev = m.to_device()
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    ms = [2, 6, 16]
+    others = np.array([i for i in range(e) if i not in (2, 5)])
+    t_avoid = np.sort(np.stack([rng.choice(others, k, replace=False) for _ in range(len(x))]), axis=1)
+    t_hit = np.sort(np.stack([np.array([2, rng.choice(others)]) for _ in range(len(x))]), axis=1)
+    for truth, expect_flags in ((t_avoid, False), (t_hit, True)):
+        cnt, fcount, _ = dev.evaluate(xt, torch.from_numpy(truth), k, ms)
+        c = pb.EvalCounters.from_array(cnt.cpu().numpy(), k, e, ms)
+        oc = O.eval_counters(zref, truth, e, ms)
+        assert c.top1 == oc["top1_count"] and c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
+        assert np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
+        nflag = int(fcount.item())
+        assert (nflag > 0) == expect_flags, nflag
+
+
 def test_nonfinite_input_raises(pb, O):
     m = bf16_model(pb, O, "arch2", 64, 128, 16, seed=1)
     x = np.zeros((4, 64))
