@@ -149,8 +149,7 @@ eval_reg_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict
     for (int r = 0; r < RPI; ++r) {
       if (base + r * RPW >= n) break;  // warp-uniform
       const bool ok = base + r * RPW + sub < n;
-      int my_rank = 0, any0 = 0;
-      int inside[MOEP_MAX_BOUNDS] = {0, 0, 0, 0};
+      int my_rank = 0;
       for (int j = 0; j < k; ++j) {
         const int t = __shfl_sync(0xffffffffu, tv[r], j, LPR);
         const T zt = __shfl_sync(0xffffffffu, lane_pick<T, EPL>(zv[r], t / LPR), t % LPR, LPR);
@@ -161,10 +160,14 @@ eval_reg_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict
           rk += __popc(__ballot_sync(0xffffffffu, e < E && key_gt(zv[r][i], e, zt, t)) & submask);
         }
         if (li == j) my_rank = rk;
-        any0 |= rk == 0;
-#pragma unroll
-        for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) inside[mi] += rk < m_of[mi] ? 1 : 0;
       }
+      // lane j < k holds true expert j's rank: the per-token counts are ballots
+      const bool mine = li < k;
+      const int any0 = (__ballot_sync(0xffffffffu, mine && my_rank == 0) & submask) != 0;
+      int inside[MOEP_MAX_BOUNDS];
+#pragma unroll
+      for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi)
+        inside[mi] = __popc(__ballot_sync(0xffffffffu, mine && my_rank < m_of[mi]) & submask);
       // true ids of a token are distinct: lanes j < k of a token update
       // different bins; the tokens of a warp use their own hist copies in turn
       for (int g = 0; g < RPW; ++g) {
