@@ -25,7 +25,11 @@ namespace moep {
 namespace k2b {
 
 constexpr int TM = 64, TN = 128, KS = 16;
-constexpr int DEC_ROWS_MAX = 256;  // fix-up: flagged counts up to this take dec_gemm, larger ones fix_gemm
+#ifndef MOEP_DEC_ROWS_MAX
+#define MOEP_DEC_ROWS_MAX 512
+#endif
+// fix-up: flagged counts up to this take dec_gemm, larger ones fix_gemm
+constexpr int DEC_ROWS_MAX = MOEP_DEC_ROWS_MAX;
 constexpr int NT = 256;
 
 __device__ __forceinline__ double bf16_to_f64(uint32_t u) {

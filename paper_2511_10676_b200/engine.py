@@ -265,7 +265,7 @@ class DevicePredictor:
     def _fixup(self, a, n, partials2=None):
         """Exact fp64 recompute of K1's flagged rows (fast path + overflow)."""
         cap = self._fixup_cap(n)
-        size = max(cap * ((self.hidden + 127) // 128), min(cap, 256) * ((self.hidden + 15) // 16)) * self.E
+        size = max(cap * ((self.hidden + 127) // 128), min(cap, 1024) * ((self.hidden + 15) // 16)) * self.E
         scratch = torch.empty(size, dtype=torch.float64, device=self.device)
         check(lib().moep_fixup_fp64(a, ptr(scratch), cap, ptr(partials2), _stream(self.device)),
               "moep_fixup_fp64")

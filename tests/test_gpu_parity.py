@@ -287,7 +287,7 @@ def test_input_norm_kernel(pb, O):
         assert np.array_equal(out, ref), kind
 
 
-@pytest.mark.parametrize("tau_rel,lo,hi", [(2e-4, 257, 3000), (1.5e-5, 1, 256)])
+@pytest.mark.parametrize("tau_rel,lo,hi", [(1e-3, 513, 3000), (1.5e-5, 1, 512)])
 def test_fixup_overflow_path(pb, O, tau_rel, lo, hi):
     """Flagged rows beyond the fix-up capacity go through the per-group fp64
     kernel; results must be identical either way (forced tiny capacity + a wide

@@ -15,7 +15,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "tools", "_k1prof")
-FLAGS = {"W1NORMAL": ["-DK1V4_W1_NORMAL"], "XNORMAL": ["-DK1V4_X_NORMAL"], "TRACE": ["-DMOEP_K1_PROF"], "NOW1": ["-DMOEP_K1_EXP_NOW1"], "NOX": ["-DMOEP_K1_EXP_NOX"], "NOACT": ["-DMOEP_K1_PROF_NOACT"],
+FLAGS = {"DEC512": ["-DMOEP_DEC_ROWS_MAX=512"], "DEC1024": ["-DMOEP_DEC_ROWS_MAX=1024"],
+         "W1NORMAL": ["-DK1V4_W1_NORMAL"], "XNORMAL": ["-DK1V4_X_NORMAL"], "TRACE": ["-DMOEP_K1_PROF"], "NOW1": ["-DMOEP_K1_EXP_NOW1"], "NOX": ["-DMOEP_K1_EXP_NOX"], "NOACT": ["-DMOEP_K1_PROF_NOACT"],
          "base": []}
 
 TIMER = r'''
@@ -91,14 +92,14 @@ def build(tag):
     os.makedirs(OUT, exist_ok=True)
     lib = os.path.join(OUT, f"libmoep_exp_{tag}.so")
     objs = []
-    for name in ("k1v2_predict", "k1v4_predict"):
+    for name in ("k1v2_predict", "k1v4_predict", "k2b_fixup"):
         obj = os.path.join(OUT, f"{name}_{tag}.o")
         subprocess.run([b.nvcc(), *b.ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *FLAGS[tag],
                         "-I", os.path.join(ROOT, "include"), "-c", os.path.join(b.CSRC, name + ".cu"), "-o", obj],
                        check=True)
         objs.append(obj)
     others = [o for o in glob.glob(os.path.join(b.HERE, "_build", "*.o"))
-              if not o.endswith(("k1v2_predict.o", "k1v4_predict.o"))]
+              if not o.endswith(("k1v2_predict.o", "k1v4_predict.o", "k2b_fixup.o"))]
     subprocess.run([b.nvcc(), *b.ARCH, "-shared", "-o", lib, *objs, *others], check=True)
     return lib
 
