@@ -306,6 +306,9 @@ int moep_teacher_normals(uint64_t seed, int64_t first_index, int64_t n, int32_t 
  * reduction order (0 + pairwise_sum) and single roundings: bit-identical to
  * numpy. out may alias x. */
 int moep_layer_norm_np(const double* x, int64_t n, int32_t d, double eps, double* out, void* stream);
+/* core.softmax (core.py:19-24) over the rows of an fp64 [n, E] array in
+ * numpy's order (max, exp, 0 + pairwise_sum, divide); out may alias z. */
+int moep_softmax_np(const double* z, int64_t n, int32_t E, double* out, void* stream);
 /* gate softmax (core.py:19-24) of fp64 logits [n, E] in numpy order, float32
  * scores [n, E] and ascending top-k ids [n, k] of the float32 scores
  * (make_dataset, synthgen.py:148-159; core.py:42-48). E <= 256. */

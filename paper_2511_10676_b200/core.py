@@ -3,8 +3,9 @@
 `top_k`, `top_k_batch` and `rank_order` keep the reference contract — stable
 descending order, ties to the lower index, `top_k*` returned ascending
 (core.py:27-54) — and run on the GPU through K7 (`moep_topk_logits`).
-`softmax` is a small fp64 torch helper on the device; `layer_norm` runs the
-K11b kernel with numpy's summation order (bit-identical to the reference). numpy in -> numpy out; CUDA tensors in -> CUDA tensors out.
+`softmax` and `layer_norm` run K11 kernels with numpy's reduction order
+(`layer_norm` bit-identical to the reference; `softmax` to within CUDA's vs
+numpy's exp ulp). numpy in -> numpy out; CUDA tensors in -> CUDA tensors out.
 """
 
 from __future__ import annotations
@@ -27,11 +28,18 @@ def _to_device(a, dtype=torch.float64):
 
 
 def softmax(logits, axis: int = -1):
-    """Max-subtracted softmax (core.py:19-24), fp64."""
+    """Max-subtracted softmax (core.py:19-24), fp64, in numpy's reduction order
+    (K11 `moep_softmax_np`; any axis is moved last first)."""
+    from ._lib import check, lib, ptr
     z, is_t = _to_device(logits)
-    z = z - z.amax(dim=axis, keepdim=True)
-    e = torch.exp(z)
-    out = e / e.sum(dim=axis, keepdim=True)
+    zm = torch.movedim(z, axis, -1).contiguous()
+    shape = zm.shape
+    flat = zm.reshape(-1, shape[-1])
+    out = torch.empty_like(flat)
+    if flat.numel() > 0:
+        check(lib().moep_softmax_np(ptr(flat), flat.shape[0], flat.shape[1], ptr(out),
+                                    torch.cuda.current_stream(flat.device).cuda_stream), "moep_softmax_np")
+    out = torch.movedim(out.reshape(shape), -1, axis)
     return out if is_t else out.cpu().numpy()
 
 

@@ -16,6 +16,8 @@
 //                          var = pairwise((x - mean)^2) / d, (x - mean) /
 //                          sqrt(var + eps) — every operation rounded once
 //                          (explicit _rn intrinsics, no FMA contraction).
+//   moep_softmax_np        core.softmax (core.py:19-24) over fp64 rows in numpy's
+//                          order (max, exp, pairwise sum, divide).
 //   moep_teacher_finish    softmax (core.py:19-24) in numpy order, float32 cast
 //                          and top-k of the float32 scores (make_dataset,
 //                          synthgen.py:148-159; core.py:42-48: descending,
@@ -364,6 +366,44 @@ __global__ void teacher_finish_kernel(const double* __restrict__ logits, int64_t
   }
 }
 
+// core.softmax (core.py:19-24) over fp64 rows in numpy's order: max,
+// subtract, exp, 0 + pairwise_sum, divide. One warp per row, the row staged
+// in shared memory (any E up to the plan's leaf capacity).
+__global__ void softmax_np_kernel(const double* __restrict__ z, int64_t n, int E, double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  PwPlan& plan = *reinterpret_cast<PwPlan*>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int row_words = pad(E - 1) + 1;
+  const int LEN = E;
+  double* base = reinterpret_cast<double*>(smem + ((sizeof(PwPlan) + 15) & ~size_t(15)));
+  double* row = base + static_cast<size_t>(warp) * (row_words + leaf_cap(LEN));
+  double* leafsum = row + row_words;
+  if (threadIdx.x == 0) {
+    plan.n_leaves = 0;
+    plan.n_prog = 0;
+    pw_build(plan, 0, E);
+  }
+  __syncthreads();
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * nwarps + warp; r < n; r += static_cast<int64_t>(gridDim.x) * nwarps) {
+    const double* zr = z + r * E;
+    double mx = -INFINITY;
+    for (int e = lane; e < E; e += 32) {
+      const double v = zr[e];
+      row[pad(e)] = v;
+      mx = fmax(mx, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __syncwarp();
+    for (int e = lane; e < E; e += 32) row[pad(e)] = exp(__dsub_rn(row[pad(e)], mx));
+    __syncwarp();
+    const double se = warp_pairwise<0>(row, plan, 0.0, leafsum, lane);
+    double* orow = out + r * E;
+    for (int e = lane; e < E; e += 32) orow[e] = __ddiv_rn(row[pad(e)], se);
+    __syncwarp();
+  }
+}
+
 size_t plan_smem(int nwarps, int len) {
   return ((sizeof(PwPlan) + 15) & ~size_t(15)) +
          static_cast<size_t>(nwarps) * static_cast<size_t>(pad(len - 1) + 1 + leaf_cap(len)) * sizeof(double);
@@ -426,6 +466,23 @@ int moep_teacher_finish(const double* logits, int64_t n, int32_t n_experts, int3
   else if (n_experts <= 128) MOEP_K11F(4);
   else MOEP_K11F(8);
 #undef MOEP_K11F
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+int moep_softmax_np(const double* z, int64_t n, int32_t E, double* out, void* stream) {
+  if (n <= 0 || E <= 0) return MOEP_ESHAPE;
+  if (leaf_cap(E) > kMaxLeaves) return MOEP_EUNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int nwarps = 8;
+  while (nwarps > 1 && plan_smem(nwarps, E) > 200 * 1024) --nwarps;
+  const size_t sm = plan_smem(nwarps, E);
+  if (sm > 227 * 1024) return MOEP_EUNSUPPORTED;
+  if (cudaFuncSetAttribute(softmax_np_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sm)) != cudaSuccess)
+    return MOEP_ELAUNCH;
+  const int64_t want = (n + nwarps - 1) / nwarps;
+  const int grid = static_cast<int>(want < 8 * moep_num_sms() ? want : 8 * moep_num_sms());
+  softmax_np_kernel<<<grid, nwarps * 32, sm, st>>>(z, n, E, out);
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }
 

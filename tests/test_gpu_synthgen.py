@@ -114,3 +114,19 @@ def test_teacher_errors(sg):
         sg.RouterSpec(16, 4, 5, np.ones((4, 16)))
     with pytest.raises(ValueError):
         sg.generate_dataset(sg.TeacherSpec(r), 0)
+
+
+def test_softmax_numpy_order():
+    """core.softmax (core.py:19-24) on the device: within an ulp of numpy (CUDA
+    exp vs numpy's SIMD exp), any axis, and ranking-preserving like the
+    reference's test (test_core.py:134-147)."""
+    import paper_2511_10676_b200 as pb
+    from oracle import synthgen as S
+    rng = np.random.default_rng(5)
+    for shape, axis in [((1000, 64), -1), ((300, 128), 0), ((4, 7, 33), 1), ((2, 5000), -1)]:
+        z = rng.standard_normal(shape) * 4
+        got = pb.softmax(z, axis=axis)
+        want = np.moveaxis(S.softmax(np.moveaxis(z, axis, -1)), -1, axis)
+        np.testing.assert_allclose(got, want, rtol=4e-16 * 8, atol=0)
+    z = rng.standard_normal((1000, 64))
+    assert np.array_equal(np.argsort(-pb.softmax(z), axis=1, kind="stable"), np.argsort(-z, axis=1, kind="stable"))
