@@ -105,7 +105,7 @@ def device_loss(spec: LossSpec, z: torch.Tensor, scores: torch.Tensor, mask_u8: 
     sums across ranks before the global normalisers are applied."""
     dev = z.device
     n, e = z.shape
-    nblk = max(1, min(lib().moep_num_sms() * 2, (n + 7) // 8))
+    nblk = max(1, min(lib().moep_num_sms() * 8, (n + 7) // 8))  # enough warps to hide the per-token chains
     dz = torch.empty_like(z)
     code = FAMILY_CODE[spec.family] if family_code is None else family_code
     dzh = torch.empty_like(z) if code >= 3 else None
