@@ -788,7 +788,7 @@ int moep_labels(const void* scores, int32_t dtype, int64_t n, int32_t E, int32_t
   if (n <= 0 || E <= 0) return MOEP_ESHAPE;
   if (k < 1 || k > E) return MOEP_EARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int grid = moep_num_sms() * 4;
+  const int grid = moep_num_sms() * 8;  // 8 CTAs of 256 per SM: hide the per-token shuffle chains
   const int top_cut = E < 10 ? E : 10;  // TOP_TIER_SIZE (losses.py:27)
   if (E <= 256) {
 #define MOEP_K3(T, LPR, EPL)                                                                                \
