@@ -718,6 +718,9 @@ dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
 #pragma unroll
     for (int s4 = 0; s4 < 4; ++s4) {
       const int k = c * DKC + kw + s4 * 4 + q4;
+      // F2F (XU pipe) conversions: measured faster here than integer-pipe
+      // rebias or a DMUL-by-2^896 rebias (both slow the DMMA issue: 240 vs
+      // 261-267 us per 1 M-token layer at ~490 flagged rows)
       double av[MT], bv[2];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -822,6 +825,10 @@ static int launch_dec(const moep_fp64_args* a, int64_t cap, double* scratch, cud
     return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
   };
   constexpr size_t kSmemMax = 227 * 1024;
+  // one CTA per SM either way (full-K staging): 32-token tiles issue 8 DMMAs
+  // per 6 operand loads (16-token tiles: 4 per 4) and halve the W1 re-reads
+  if (bulk_ok && grid_rows > 32 && dec_bulk_smem<32>(a->d, a->n_experts) <= kSmemMax)
+    return gob(dec_gemm_bulk<32>, 32, dec_bulk_smem<32>(a->d, a->n_experts));
   if (bulk_ok && grid_rows > 8 && dec_bulk_smem<16>(a->d, a->n_experts) <= kSmemMax)
     return gob(dec_gemm_bulk<16>, 16, dec_bulk_smem<16>(a->d, a->n_experts));
   if (bulk_ok && grid_rows <= 8 && dec_bulk_smem<8>(a->d, a->n_experts) <= kSmemMax)

@@ -88,3 +88,32 @@ def test_tensor_core_path_forced_small_batches(pb, O, n):
     dev.decode_max_tokens = 0
     xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
     assert np.array_equal(dev.topk(xt, 8).cpu().numpy(), O.top_k_batch(zref, 8))
+
+
+@pytest.mark.parametrize("n", [12, 40])
+def test_decode_zero_and_subnormal_bf16_operands(pb, O, n):
+    """The DMMA operand conversion (bits into the fp64 hi word, one exact DMUL by
+    2^896) keeps bf16 zeros and subnormals exact: rows made only of subnormals
+    give logits of order 1e-39 whose ranking a flush-to-zero would lose."""
+    rng = np.random.default_rng(n)
+    d, h, e, k = 2048, 2048, 64, 6
+    m = bf16_model(pb, O, "arch2", d, h, e, seed=3, rng=rng)
+    w1 = m.w1.copy()
+    w1[:, ::7] = 0.0                                   # exact zeros in W1
+    w1[::5, 3::11] = rng.integers(1, 128, w1[::5, 3::11].shape) * 2.0 ** -133  # W1 subnormals
+    m.w1 = w1
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    sub = rng.integers(1, 128, (4, d)) * 2.0 ** -133 * rng.choice([-1.0, 1.0], (4, d))
+    x[:4] = sub                                        # rows of bf16 subnormals only
+    x[4:8, ::3] = 0.0                                  # zeros mixed into normal rows
+    x[8, :] = 0.0                                      # an all-zero row
+    assert np.array_equal(O.round_bf16(x), x)
+    zref = O.predict_logits(oracle_params(m), x)
+    assert np.abs(zref[:4]).max() < 1e-30 and np.abs(zref[:4]).max() > 0
+    dev = m.to_device()
+    xt = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    assert np.array_equal(xt.cpu().double().numpy(), x)
+    z = dev.logits(xt, validate=False).cpu().numpy()
+    assert np.allclose(z[:4], zref[:4], rtol=1e-9, atol=0), np.abs(z[:4] - zref[:4]).max()
+    assert np.allclose(z, zref, rtol=0, atol=1e-11), np.abs(z - zref).max()
+    assert np.array_equal(dev.topk(xt, k, validate=False).cpu().numpy(), O.top_k_batch(zref, k))
