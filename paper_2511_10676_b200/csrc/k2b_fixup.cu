@@ -498,6 +498,13 @@ dec_finish(moep_fp64_args a, int64_t cap, int ntile, const double* __restrict__ 
 // summed in fixed order, then bias + activation (predictor.py:193-240) and the
 // W2 partial of this CTA's hidden units -> part[(row * ntile + tile) * E + e].
 constexpr int DH = 16, DKC = 128;
+#ifndef MOEP_DEC_BIG_NW
+#define MOEP_DEC_BIG_NW 8
+#endif
+// warps of the 32-token bulk kernel (one CTA per SM). 16 warps (each K chunk
+// split 16 ways) measured slower: 309 vs 240 us per 1 M-token layer at ~490
+// flagged rows (profiles/r01_fixup_dec_gemm_bulk_ncu.csv)
+constexpr int DEC_BIG_NW = MOEP_DEC_BIG_NW;
 
 template <int XT, int WT, int TT>
 __global__ void __launch_bounds__(256)
@@ -648,10 +655,11 @@ dec_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
 // per-chunk mbarriers, so the HBM latency is paid once instead of per chunk.
 // Warp w converts and consumes only K columns 16w..16w+15 of each chunk, so
 // the K loop needs no CTA-wide barrier.
-template <int TT>
-__global__ void __launch_bounds__(256)
+template <int TT, int NW>
+__global__ void __launch_bounds__(32 * NW)
 dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
-  static_assert(TT % 8 == 0 && DH == 16, "tile");
+  static_assert(TT % 8 == 0 && DH == 16 && (NW == 8 || NW == 16), "tile");
+  constexpr int NTH = 32 * NW, KW = DKC / NW;  // threads; K columns per warp per chunk
   extern __shared__ __align__(128) uint8_t smb[];
   const int d = a.d, H = a.hidden, E = a.n_experts;
   const int rp = d + 8;                        // raw bf16 row pitch (16 B pad: 4-bank shift per row)
@@ -659,7 +667,7 @@ dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   uint16_t* wraw = reinterpret_cast<uint16_t*>(smb);            // [DH][rp]
   uint16_t* xraw = wraw + DH * rp;                               // [TT][rp]
   size_t rawb = sizeof(uint16_t) * (DH + TT) * rp;                // same layout as dec_bulk_smem
-  if (rawb < sizeof(double) * 9 * TT * DH) rawb = sizeof(double) * 9 * TT * DH;
+  if (rawb < sizeof(double) * (NW + 1) * TT * DH) rawb = sizeof(double) * (NW + 1) * TT * DH;
   rawb = (rawb + 15) & ~static_cast<size_t>(15);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smb + rawb);        // [nseg]
   uint16_t* w2smem = (E % 8 == 0) ? reinterpret_cast<uint16_t*>(bars + 4) : nullptr;  // [DH][E]
@@ -693,7 +701,7 @@ dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
     const int R = nv + hv;
     const uint16_t* xg = reinterpret_cast<const uint16_t*>(a.x);
     const uint16_t* wg = reinterpret_cast<const uint16_t*>(a.w1);
-    for (int q = tid; q < R * nseg; q += 256) {
+    for (int q = tid; q < R * nseg; q += NTH) {
       const int r = q % R, c = q / R;
       if (r < nv)
         bulk_g2s(xraw + r * rp + c * segk, xg + rowid[r] * d + c * segk, segk * 2, &bars[c]);
@@ -712,11 +720,11 @@ dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-  const int kw = warp * 16;                    // this warp's 16 columns of every chunk
+  const int kw = warp * KW;                    // this warp's KW columns of every chunk
   for (int c = 0; c < nk; ++c) {
     if (c % cps == 0) mbar_wait(&bars[c / cps], 0);
 #pragma unroll
-    for (int s4 = 0; s4 < 4; ++s4) {
+    for (int s4 = 0; s4 < KW / 4; ++s4) {
       const int k = c * DKC + kw + s4 * 4 + q4;
       // F2F (XU pipe) conversions: measured faster here than integer-pipe
       // rebias or a DMUL-by-2^896 rebias (both slow the DMMA issue: 240 vs
@@ -751,12 +759,12 @@ dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
       for (int hh = 0; hh < 2; ++hh)
         red[(warp * TT + g + 8 * mt) * DH + 8 * nt + 2 * q4 + hh] = acc[mt][nt][hh];
   __syncthreads();
-  double* hs = red + 8 * TT * DH;              // [TT][DH]
-  for (int o = tid; o < TT * DH; o += 256) {
+  double* hs = red + NW * TT * DH;             // [TT][DH]
+  for (int o = tid; o < TT * DH; o += NTH) {
     const int t = o / DH, j = o % DH, jg = h0 + j;
     double sum = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) sum += red[(w * TT + t) * DH + j];
+    for (int w = 0; w < NW; ++w) sum += red[(w * TT + t) * DH + j];
     double hval = 0.0;
     if (jg < H && rowid[t] >= 0) {
       const double av = sum + a.b1[jg];
@@ -775,7 +783,7 @@ dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   // with the first K segment when E % 8 == 0) are reused for every token
   const uint16_t* w2t = reinterpret_cast<const uint16_t*>(a.w2t);
   const uint16_t* w2s = w2smem ? w2smem : w2t + static_cast<int64_t>(h0) * E;
-  for (int e = tid; e < E; e += 256) {
+  for (int e = tid; e < E; e += NTH) {
     double wv[DH];
 #pragma unroll
     for (int j = 0; j < DH; ++j) {
@@ -792,12 +800,12 @@ dec_gemm_bulk(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   }
 }
 
-template <int TT>
+template <int TT, int NW>
 static size_t dec_bulk_smem(int d, int E) {
   // raw rows + barriers + W2^T slice; the epilogue's warp partials + hidden tile
   // (9 * TT * DH doubles) reuse the raw rows and must not reach the W2 slice
   size_t raw = sizeof(uint16_t) * (DH + TT) * (d + 8);
-  const size_t red = sizeof(double) * 9 * TT * DH;
+  const size_t red = sizeof(double) * (NW + 1) * TT * DH;
   if (raw < red) raw = red;
   raw = (raw + 15) & ~static_cast<size_t>(15);
   return raw + sizeof(uint64_t) * 4 + sizeof(uint16_t) * DH * E;
@@ -817,22 +825,22 @@ static int launch_dec(const moep_fp64_args* a, int64_t cap, double* scratch, cud
   // bulk-copy kernel: bf16 x and W1, d a multiple of DKC, 16-byte aligned rows
   const bool bulk_ok = xb && wb && (a->d % DKC) == 0 && (reinterpret_cast<uintptr_t>(a->x) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(a->w1) & 15) == 0;
-  auto gob = [&](auto kern, int tt, size_t smem) {
+  auto gob = [&](auto kern, int tt, int nw, size_t smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
       return MOEP_ELAUNCH;
     dim3 grid(static_cast<unsigned>(ntile), static_cast<unsigned>((grid_rows + tt - 1) / tt));
-    kern<<<grid, 256, smem, st>>>(*a, cap, scratch);
+    kern<<<grid, 32 * nw, smem, st>>>(*a, cap, scratch);
     return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
   };
   constexpr size_t kSmemMax = 227 * 1024;
   // one CTA per SM either way (full-K staging): 32-token tiles issue 8 DMMAs
   // per 6 operand loads (16-token tiles: 4 per 4) and halve the W1 re-reads
-  if (bulk_ok && grid_rows > 32 && dec_bulk_smem<32>(a->d, a->n_experts) <= kSmemMax)
-    return gob(dec_gemm_bulk<32>, 32, dec_bulk_smem<32>(a->d, a->n_experts));
-  if (bulk_ok && grid_rows > 8 && dec_bulk_smem<16>(a->d, a->n_experts) <= kSmemMax)
-    return gob(dec_gemm_bulk<16>, 16, dec_bulk_smem<16>(a->d, a->n_experts));
-  if (bulk_ok && grid_rows <= 8 && dec_bulk_smem<8>(a->d, a->n_experts) <= kSmemMax)
-    return gob(dec_gemm_bulk<8>, 8, dec_bulk_smem<8>(a->d, a->n_experts));
+  if (bulk_ok && grid_rows > 32 && dec_bulk_smem<32, DEC_BIG_NW>(a->d, a->n_experts) <= kSmemMax)
+    return gob(dec_gemm_bulk<32, DEC_BIG_NW>, 32, DEC_BIG_NW, dec_bulk_smem<32, DEC_BIG_NW>(a->d, a->n_experts));
+  if (bulk_ok && grid_rows > 8 && dec_bulk_smem<16, 8>(a->d, a->n_experts) <= kSmemMax)
+    return gob(dec_gemm_bulk<16, 8>, 16, 8, dec_bulk_smem<16, 8>(a->d, a->n_experts));
+  if (bulk_ok && grid_rows <= 8 && dec_bulk_smem<8, 8>(a->d, a->n_experts) <= kSmemMax)
+    return gob(dec_gemm_bulk<8, 8>, 8, 8, dec_bulk_smem<8, 8>(a->d, a->n_experts));
   auto go = [&](auto kern, int tt) {
     const size_t smem = sizeof(double) * 2 * DKC * (tt + DH);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
