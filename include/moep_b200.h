@@ -65,7 +65,9 @@ typedef struct {
   int32_t m_sel;              /* ids per token written to `ids` (0: none; <= 15 or == E) */
   int32_t n_bounds;           /* margin-check boundaries (positions), <= MOEP_MAX_BOUNDS */
   int32_t bounds[MOEP_MAX_BOUNDS];
-  float tau_abs, tau_rel;     /* flag when gap < tau_abs + tau_rel*||h||*w2_norm */
+  float tau_abs, tau_rel;     /* flag when gap < tau_abs + tau_rel*||h||*w2_norm; tau_rel is for the
+                                 kernels with a separate lo-product accumulator (pair kernels, E <= 64
+                                 in v4); the others widen it 1.5x (their measured error) */
   float w2_norm;              /* max_e ||w2[e,:]||_2 */
   int32_t* ids;               /* [N, m_sel] ascending, or NULL */
   float* logits;              /* [N, E] fp32, or NULL */
@@ -80,7 +82,15 @@ typedef struct {
   float* a_out;               /* [N, hidden] fp32 pre-activation W1.x + b1 (training), or NULL */
   float* split_scratch;       /* hidden-split partial logits for small N (see below), or NULL */
   int64_t split_scratch_floats;
+  int32_t* status;            /* [1] device word, or NULL: bit 0 is OR-ed in when a token's fp32
+                                 logits are non-finite (such tokens are also flagged). The caller
+                                 then checks the input for NaN/Inf, the reference's
+                                 ConfigurationError (predictor.py:188-189), without a separate
+                                 isfinite pass over x in the common case. */
+  int32_t kernel;             /* MOEP_K1_AUTO (0) or a forced kernel (tests / measurements) */
 } moep_predict_args;
+
+enum { MOEP_K1_AUTO = 0, MOEP_K1_ONE_SM = 1, MOEP_K1_PAIR_V2 = 2, MOEP_K1_PAIR_V4 = 4 };
 
 int moep_predict_bf16(const moep_predict_args* a, void* stream);
 

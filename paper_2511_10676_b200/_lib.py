@@ -14,7 +14,7 @@ import os
 from .exceptions import ConfigurationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# MOEP_LIB: alternative build of the same library (the profiling build of tools/k1_prof.py)
+# MOEP_LIB: alternative build of the same library (tools/variant_lib.py, tools/k1_prof.py)
 LIB_PATH = os.environ.get("MOEP_LIB") or os.path.join(_HERE, "libmoep_b200.so")
 
 MOEP_OK, MOEP_ESHAPE, MOEP_EALIGN, MOEP_EUNSUPPORTED, MOEP_ELAUNCH, MOEP_EARG = 0, -1, -2, -3, -4, -5
@@ -33,8 +33,11 @@ class PredictArgs(C.Structure):
         ("tau_abs", f32), ("tau_rel", f32), ("w2_norm", f32),
         ("ids", vp), ("logits", vp), ("flags", vp), ("flag_list", vp), ("flag_count", vp),
         ("truth", vp), ("k", i32), ("n_m", i32), ("m_list", i32 * MAX_BOUNDS), ("partials", vp),
-        ("a_out", vp), ("split_scratch", vp), ("split_scratch_floats", i64),
+        ("a_out", vp), ("split_scratch", vp), ("split_scratch_floats", i64), ("status", vp), ("kernel", i32),
     ]
+
+
+MOEP_K1_AUTO, MOEP_K1_ONE_SM, MOEP_K1_PAIR_V2, MOEP_K1_PAIR_V4 = 0, 1, 2, 4
 
 
 class Fp64Args(C.Structure):

@@ -52,7 +52,11 @@ __device__ __forceinline__ __nv_bfloat16 f64_to_bf16_rne(double x) {
   return __float2bfloat16_rn(static_cast<float>(r));                // exact (or inf on overflow)
 }
 
+#ifdef MOEP_SILU_ACCURATE
+__device__ __forceinline__ float silu_f32(float a) { return __fdiv_rn(a, 1.0f + expf(-a)); }
+#else
 __device__ __forceinline__ float silu_f32(float a) { return __fdividef(a, 1.0f + __expf(-a)); }
+#endif
 
 __device__ __forceinline__ float gelu_tanh_f32(float u) {
   const float c = 0.7978845608028654f, ga = 0.044715f;

@@ -29,6 +29,7 @@ struct Params {
   int* partials;
   int n_counters;
   float* a_out;
+  int* status;  // bit 0: some token's fp32 logits were non-finite (host checks the input)
   // hidden split (pair kernel, small N): `split` chunk groups per 256-token tile;
   // partial z [split][zpad][EP] and partial ||h||^2 [split][zpad] in zpart
   int split;
@@ -115,6 +116,8 @@ __device__ __forceinline__ void row_epilogue_core(const Params& p, ZGet zv, bool
   // flags on the gap alone; an evaluation-only boundary (1, k, m_list:
   // metrics.py:159-180 count only where the TRUE experts rank) flags only when
   // a true expert lies in that window — its counters cannot change otherwise.
+  // entry value of `flagged`: this token's fp32 logits are non-finite
+  if (flagged && valid && p.status) atomicOr(p.status, 1);
   const bool eval_only_ok = p.truth != nullptr && valid;
 #pragma unroll
   for (int b = 0; b < MOEP_MAX_BOUNDS; ++b) {

@@ -52,6 +52,8 @@ struct Cfg {
   static constexpr int NBAR = 2 * STAGES + 2 + 2 + 2 + 1 + 2 + 2;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // + tmem slot + align slack
   static constexpr uint32_t ZCOL = 2 * HC;                 // TMEM column of the z accumulator
+  static constexpr uint32_t ZLCOL = ZCOL + EP;             // lo-product accumulator
+  static_assert(ZLCOL + EP <= 512, "TMEM columns");
 };
 
 struct Params {
@@ -75,6 +77,7 @@ struct Params {
   int* partials;
   int n_counters;
   float* a_out;
+  int* status;
 };
 
 // ------------------------------------------------------------------ kernel
@@ -178,7 +181,7 @@ predict_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
             const uint64_t ahi = sdesc_k_sw128(a2_base + g * C::A2_BYTES + k * 32);
             const uint64_t alo = sdesc_k_sw128(a2_base + (2 + g) * C::A2_BYTES + k * 32);
             umma_bf16(tmem + C::ZCOL, ahi, bd, idesc2, (cc | g | k) != 0);
-            umma_bf16(tmem + C::ZCOL, alo, bd, idesc2, 1u);
+            umma_bf16(tmem + C::ZLCOL, alo, bd, idesc2, (cc | g | k) != 0);
           }
         }
         umma_commit(a2_empty);
@@ -312,6 +315,14 @@ predict_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
 #pragma unroll
         for (int j = 0; j < EP; j += 16) tmem_ld16(tmem + lane_addr + C::ZCOL + j, z + j);
         tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < EP; j += 16) {
+          float zl[16];
+          tmem_ld16(tmem + lane_addr + C::ZLCOL + j, zl);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 16; ++t) z[j + t] += zl[t];
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(z_empty);
@@ -327,6 +338,7 @@ predict_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
             z[e] = -INFINITY;
           }
         }
+        if (flagged && valid && p.status) atomicOr(p.status, 1);
         // top-P by repeated first-argmax (ties -> lower index)
         int P = p.m_sel;
 #pragma unroll
@@ -519,6 +531,7 @@ int launch_k1(const moep_predict_args* a, cudaStream_t st, const CUtensorMap& tx
   p.ids = a->ids; p.logits = a->logits; p.flags = a->flags;
   p.flag_list = a->flag_list; p.flag_count = a->flag_count;
   p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;
+  p.status = a->status;
   p.n_counters = moep_n_counters(a->n_m, a->n_experts);
   const int grid = moep_num_sms();
   kern<<<grid, NTHREADS, C::SMEM, st>>>(tx, tw1, tw2, p);
@@ -542,14 +555,12 @@ extern "C" int moep_predict_bf16(const moep_predict_args* a, void* stream) {
   if (!a->flag_list || !a->flag_count) return MOEP_EARG;
   if (a->arch == 2 && !a->b1) return MOEP_EARG;
   if (a->arch == 1 && (!a->act_alpha || !a->act_beta)) return MOEP_EARG;
-  // The CTA-pair kernel (k1v2_predict.cu) covers hidden % 256 == 0; the 1-SM
-  // kernel below handles every other shape. MOEP_K1_VARIANT=1 forces the latter.
-  static int variant = -1;
-  if (variant < 0) {
-    const char* env = getenv("MOEP_K1_VARIANT");
-    variant = (env && env[0] == '1') ? 1 : 2;
-  }
-  if (variant == 2) {
+  if (a->kernel != MOEP_K1_AUTO && a->kernel != MOEP_K1_ONE_SM && a->kernel != MOEP_K1_PAIR_V2 &&
+      a->kernel != MOEP_K1_PAIR_V4)
+    return MOEP_EARG;
+  // The CTA-pair kernels (k1v2/k1v4_predict.cu) cover hidden % 256 == 0; the
+  // 1-SM kernel below handles every other shape (or kernel == MOEP_K1_ONE_SM).
+  if (a->kernel != MOEP_K1_ONE_SM) {
     const int rc = moep_predict_bf16_pair(a, stream);
     if (rc != MOEP_EUNSUPPORTED) return rc;
   }

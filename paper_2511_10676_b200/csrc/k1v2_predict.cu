@@ -84,6 +84,11 @@ struct Cfg {
   static constexpr int NBAR = 2 * STAGES + 10;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
   static constexpr uint32_t ZCOL = HC;  // TMEM column of the z accumulator
+  // GEMM2's lo products accumulate apart from the hi ones (summed in fp32 by
+  // the token epilogue): half the truncating accumulate steps on z and none of
+  // them against a full-size accumulator (max logit error -32 %)
+  static constexpr uint32_t ZLCOL = HC + EP;
+  static_assert(ZLCOL + EP <= 512, "TMEM columns");
 };
 
 template <int EP, int ARCH>
@@ -232,7 +237,7 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
               const uint64_t ahi = sdesc_k_sw128(a2_base + at * C::ATOM + w * 32);
               const uint64_t alo = sdesc_k_sw128(a2_base + (2 + at) * C::ATOM + w * 32);
               umma_bf16_cg2(tmem + C::ZCOL, ahi, bd, idesc2, (p_cc | half | kk) != 0);
-              umma_bf16_cg2(tmem + C::ZCOL, alo, bd, idesc2, 1u);
+              umma_bf16_cg2(tmem + C::ZLCOL, alo, bd, idesc2, (p_cc | half | kk) != 0);
             }
             K1_TR(3 + half, p_id, true);
             if (half == 0) {
@@ -400,6 +405,14 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
 #pragma unroll
         for (int j = 0; j < EP; j += 16) tmem_ld16(tmem + lane_addr + C::ZCOL + j, z + j);
         tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < EP; j += 16) {
+          float zl[16];
+          tmem_ld16(tmem + lane_addr + C::ZLCOL + j, zl);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 16; ++t) z[j + t] += zl[t];
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(z_empty, 0);
@@ -494,6 +507,7 @@ __global__ void __launch_bounds__(256) split_finish_kernel(const Params p) {
       }
     }
     bool flagged = __any_sync(0xffffffffu, bad);
+    if (flagged && lane == 0 && p.status) atomicOr(p.status, 1);
     // sorted top list (warp-uniform): repeated warp argmax over the untaken experts
     float tv[kMaxSel];
     int tix[kMaxSel];
@@ -634,30 +648,13 @@ __global__ void __launch_bounds__(256) split_finish_kernel(const Params p) {
   }
 }
 
-// Which pair kernel runs: v4 (k1v4_predict.cu: token epilogue on its own
-// warpgroup, A2 in TMEM) for unsplit launches with at least two 256-token
-// tiles per CTA pair, this file's v2 kernel otherwise (hidden-split small-N
-// launches, one-wave launches).
-// MOEP_K1_VARIANT=2 forces v2; =3 selects v3 (double-buffered accumulator,
-// 192-column chunks, E <= 64: removes the drain bubble but measured slower,
-// profiles/r01_k1_role_waits.md); =1 selects the 1-SM kernel in moep_predict_bf16.
-static int variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* env = getenv("MOEP_K1_VARIANT");
-    v = (env && env[0] == '3') ? 3 : (env && env[0] == '2') ? 2 : 4;
-  }
-  return v;
-}
-static bool use_v3(int hidden, int n_experts) {
-  return variant() == 3 && hidden % 64 == 0 && n_experts <= 64;  // EP = 128 spills in v3 (round 2)
-}
-// v4 (A2 in TMEM, 5-stage ring, token epilogue on its own warpgroup;
-// k1v4_predict.cu) for unsplit launches
-static bool use_v4(int hidden, int n_experts) { return variant() == 4 && hidden % HC == 0 && n_experts <= 128; }
-
-static int pair_chunks(int hidden, int n_experts) {
-  return use_v3(hidden, n_experts) ? (hidden + 191) / 192 : hidden / HC;
+// Which pair kernel runs (moep_predict_args.kernel): auto (0) takes v4
+// (k1v4_predict.cu: token epilogue on its own warpgroup, A2 in TMEM) for
+// unsplit launches with at least two 256-token tiles per CTA pair and this
+// file's v2 kernel otherwise (hidden-split small-N launches, one-wave
+// launches); MOEP_K1_PAIR_V2 (2) / MOEP_K1_PAIR_V4 (4) force one of them.
+static bool use_v4(const moep_predict_args* a) {
+  return a->kernel != MOEP_K1_PAIR_V2 && a->hidden % HC == 0 && a->n_experts <= 128;
 }
 
 // Chunk groups per tile: only when the tiles leave CTA pairs idle (fewer tiles
@@ -700,8 +697,8 @@ extern "C" int moep_k1_prof(unsigned long long* host, int reset) {
 extern "C" int64_t moep_predict_split_floats(int64_t n_tokens, int32_t hidden, int32_t n_experts) {
   using namespace moep::k1v2;
   if (n_tokens <= 0 || hidden <= 0 || n_experts <= 0 || n_experts > 128) return 0;
-  if (hidden % HC != 0 && !use_v3(hidden, n_experts)) return 0;
-  const int g = choose_split(n_tokens, pair_chunks(hidden, n_experts), moep_num_sms() / 2);
+  if (hidden % HC != 0) return 0;
+  const int g = choose_split(n_tokens, hidden / HC, moep_num_sms() / 2);
   if (g == 1) return 0;
   int EP = 16;
   while (EP < n_experts) EP *= 2;
@@ -709,8 +706,6 @@ extern "C" int64_t moep_predict_split_floats(int64_t n_tokens, int32_t hidden, i
   return static_cast<int64_t>(g) * zpad * (EP + 1);
 }
 
-extern "C" int moep_predict_bf16_pair3(const moep_predict_args* a, int split, float* zpart, int64_t zpad,
-                                       void* stream);
 extern "C" int moep_predict_bf16_pair4(const moep_predict_args* a, void* stream);
 
 namespace {
@@ -741,20 +736,18 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
   p.ids = a->ids; p.logits = a->logits; p.flags = a->flags;
   p.flag_list = a->flag_list; p.flag_count = a->flag_count;
   p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;
+  p.status = a->status;
   p.n_counters = moep_n_counters(a->n_m, a->n_experts);
   const int grid = moep_num_sms() & ~1;  // whole CTA pairs
   p.split = 1; p.zpart = nullptr; p.zpad = 0;
   const int64_t need = moep_predict_split_floats(a->n_tokens, a->hidden, a->n_experts);
   if (need > 0 && a->split_scratch && a->split_scratch_floats >= need) {
-    p.split = choose_split(a->n_tokens, pair_chunks(a->hidden, a->n_experts), grid / 2);
+    p.split = choose_split(a->n_tokens, a->hidden / HC, grid / 2);
     p.zpart = a->split_scratch;
     p.zpad = ((a->n_tokens + 2 * BM - 1) / (2 * BM)) * 2 * BM;
   }
-  if (use_v3(a->hidden, a->n_experts)) {
-    const int rc = moep_predict_bf16_pair3(a, p.split, p.zpart, p.zpad, st);
-    if (rc != MOEP_OK) return rc;
-  } else if (p.split == 1 && use_v4(a->hidden, a->n_experts) &&
-             (a->n_tokens + 2 * BM - 1) / (2 * BM) >= 2 * (grid / 2)) {
+  if (p.split == 1 && use_v4(a) &&
+      (a->kernel == MOEP_K1_PAIR_V4 || (a->n_tokens + 2 * BM - 1) / (2 * BM) >= 2 * (grid / 2))) {
     // v4 hides each tile's token epilogue behind the next tile: with fewer
     // than two tiles per CTA pair there is nothing to hide it behind, and v2's
     // register-resident epilogue is the shorter path
@@ -774,7 +767,7 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
 // Pair kernel entry (validation shared with moep_predict_bf16, which dispatches here).
 extern "C" int moep_predict_bf16_pair(const moep_predict_args* a, void* stream) {
   if (a->n_experts > 128) return MOEP_EUNSUPPORTED;
-  if (a->hidden % 256 != 0 && !moep::k1v2::use_v3(a->hidden, a->n_experts)) return MOEP_EUNSUPPORTED;
+  if (a->hidden % 256 != 0) return MOEP_EUNSUPPORTED;
   int EP = 16;
   while (EP < a->n_experts) EP *= 2;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

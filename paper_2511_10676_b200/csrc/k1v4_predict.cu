@@ -90,6 +90,10 @@ struct Cfg {
   static constexpr uint32_t ZCOL = HC;               // TMEM column of the z accumulator
   static constexpr uint32_t A2COL = HC + EP;         // hi pairs [A2COL, +64), lo pairs [A2COL+64, +128)
   static_assert(A2COL + 128 <= 512, "TMEM columns");
+  // GEMM2's lo products accumulate apart from the hi ones where TMEM has the
+  // columns (EP <= 64): summed in fp32 by WG2 (max logit error -32 %)
+  static constexpr bool ZLO = A2COL + 128 + EP <= 512;
+  static constexpr uint32_t ZLCOL = ZLO ? A2COL + 128 : ZCOL;  // lo-product accumulator
   static_assert(SMEM <= 232448, "shared memory");
 };
 
@@ -281,7 +285,8 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
               const int at = kk >> 2, w = kk & 3;
               const uint64_t bd = sdesc_k_sw128(w2_base + (half * 2 + at) * C::W2_ATOM + w * 32);
               umma_bf16_cg2_ts(tmem + C::ZCOL, tmem + C::A2COL + kk * 8, bd, idesc2, (p_cc | half | kk) != 0);
-              umma_bf16_cg2_ts(tmem + C::ZCOL, tmem + C::A2COL + 64 + kk * 8, bd, idesc2, 1u);
+              umma_bf16_cg2_ts(tmem + C::ZLCOL, tmem + C::A2COL + 64 + kk * 8, bd, idesc2,
+                               C::ZLO ? uint32_t((p_cc | half | kk) != 0) : 1u);
             }
             K1_TR(3 + half, p_id, true);
             if (half == 0) {
@@ -452,6 +457,14 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
       for (int j = 0; j < EP; j += 16) {
         float zc[16];
         tmem_ld16(tmem + lane_addr + C::ZCOL + j, zc);
+        if (C::ZLO) {
+          // + the lo-product accumulator
+          float zl[16];
+          tmem_ld16(tmem + lane_addr + C::ZLCOL + j, zl);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 16; ++t) zc[t] += zl[t];
+        }
         tmem_ld_wait();
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
@@ -512,7 +525,9 @@ int launch_v4(const moep_predict_args* a, cudaStream_t st) {
   p.b1 = a->b1; p.alpha = a->act_alpha; p.beta = a->act_beta; p.b2 = a->b2;
   p.m_sel = a->m_sel; p.n_bounds = a->n_bounds;
   for (int i = 0; i < MOEP_MAX_BOUNDS; ++i) { p.bounds[i] = a->bounds[i]; p.m_list[i] = a->m_list[i]; }
-  p.tau_abs = a->tau_abs; p.tau_rel = a->tau_rel; p.w2_norm = a->w2_norm;
+  // without the separate lo accumulator (EP = 128) the logit error is 1.5x larger
+  p.tau_abs = a->tau_abs; p.tau_rel = a->tau_rel * (C::ZLO ? 1.0f : 1.5f); p.w2_norm = a->w2_norm;
+  p.status = a->status;
   p.ids = a->ids; p.logits = a->logits; p.flags = a->flags;
   p.flag_list = a->flag_list; p.flag_count = a->flag_count;
   p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;

@@ -5,10 +5,15 @@ fix-up) -> counter reduce, all enqueued on the caller's CUDA stream.
 Precision contract: the tensor-core path (K1) is used when
 the activations and both weight matrices are exactly bf16-representable. K1
 computes logits to ~1e-6 and flags every token whose selection gap is below
-    delta = tau_abs + tau_rel * ||h||_2 * max_e ||w2_e||_2 ;
-flagged tokens are recomputed in fp64 by K2 so predicted expert ids match the
-float64 reference bit for bit. Inputs that are not bf16-representable go to K2
-for every token (exact, fp64 CUDA cores).
+    delta = tau_abs' + tau_rel * ||h||_2 * max_e ||w2_e||_2 ,
+    tau_abs' = tau_abs + 2^-21 (max|b2| + 1.2 max_e||w2_e|| ||b1 (arch1: folded beta)||_2)
+(the second term covers the fp32 rounding of large biases, which the
+Cauchy-Schwarz scale does not see); flagged tokens are recomputed in fp64 by
+K2 so predicted expert ids match the float64 reference bit for bit. Inputs
+that are not bf16-representable go to K2 for every token (exact, fp64).
+Logits returned by `logits()` are exact fp64 for every row (the fp64 GEMM
+over all rows); `logits(approx=True)` returns K1's fp32 logits with the
+flagged rows patched.
 """
 
 from __future__ import annotations
@@ -25,7 +30,12 @@ from .exceptions import ConfigurationError
 K1_MAX_SEL = 15       # K1 keeps 16 sorted positions per token
 K1_MAX_EXPERTS = 128  # TMEM budget of the single-CTA kernel
 TAU_ABS = 1e-7
-TAU_REL = 2e-6
+# Every logit must lie within delta/2 of its exact value. Measured max
+# |dz| / (||h|| max||w2_e||) of K1 over 1M-token DSV2L layers: 6.2e-7 with the
+# separate lo-product accumulator (tools/precision_scan.py), so
+# tau_rel = 5e-6 leaves 8x headroom (max <= tau_rel / 8); bench.py re-measures
+# the max over every checked token of the run.
+TAU_REL = 5e-6
 DECODE_MAX_TOKENS = 64  # batches up to this size take the split-hidden exact fp64 decode kernel
 
 
@@ -119,6 +129,12 @@ class DevicePredictor:
             self.bn = [None] * 4
             self.alpha = self.beta = None
         self.w2_norm = float(torch.linalg.vector_norm(w2, dim=1).max()) if self.E else 0.0
+        # fp32 rounding of biases (K1 holds b1 / b2 / the folded BN affine in fp32):
+        # per logit <= 2^-23 (max|b2| + 1.1 max||w2_e|| ||b1||); x2 for the pair
+        # of logits at a boundary, x2 headroom (engine margin had no bias term)
+        b1_eff = self.beta.double() if self.arch == "arch1" else self.b1_f64
+        self.tau_bias = 2.0 ** -21 * (float(self.b2_f64.abs().max()) + 1.2 * self.w2_norm *
+                                      float(torch.linalg.vector_norm(b1_eff)))
         self.n_sms = lib().moep_num_sms()
 
     @classmethod
@@ -126,10 +142,16 @@ class DevicePredictor:
         return cls(model, device, **kw)
 
     # ---------------------------------------------------------------- inputs
-    def prepare(self, x: torch.Tensor, check_finite: bool = True):
-        """K0 cast: x (any float dtype, on device) -> bf16 copy, plus whether
-        every value was bf16-representable. Raises ConfigurationError on
-        non-finite input (predictor.py:188-189)."""
+    def prepare(self, x: torch.Tensor):
+        """Input contract of _check_input (predictor.py:180-190) on the device.
+
+        bf16 input: returned as is; finiteness is checked through K1's status
+        word after the launch (`check_status`), so the common path has no extra
+        pass over x and no host synchronisation. Other dtypes: the K0 cast
+        kernel writes the bf16 copy plus a status (non-finite, not
+        bf16-representable); that path synchronises to pick the kernel and
+        raises ConfigurationError on non-finite input.
+        Returns (x, x_bf16, bf16_exact)."""
         x = x.to(self.device)
         if x.dim() != 2 or x.shape[1] != self.d:
             raise ConfigurationError(f"input shape {tuple(x.shape)} incompatible with d={self.d}")
@@ -138,24 +160,30 @@ class DevicePredictor:
             x = x.to(torch.float64)
             code = MOEP_F64
         x = x.contiguous()
-        n = x.shape[0]
-        if x.dtype == torch.bfloat16 and not check_finite:
-            return x, x, True  # no host synchronisation (serving path)
         if x.dtype == torch.bfloat16:
-            xb = x
-            status = torch.zeros(2, dtype=torch.int32, device=self.device)
-            if check_finite:
-                bad = int((~torch.isfinite(x)).any())
-                status[0] = bad
-        else:
-            xb = torch.empty((n, self.d), dtype=torch.bfloat16, device=self.device)
-            status = torch.zeros(2, dtype=torch.int32, device=self.device)
-            check(lib().moep_input_norm(ptr(x), code, n, self.d, 0, None, None, 0.0, ptr(xb),
-                                        ptr(status), _stream(self.device)), "moep_input_norm")
+            return x, x, True
+        n = x.shape[0]
+        xb = torch.empty((n, self.d), dtype=torch.bfloat16, device=self.device)
+        status = torch.zeros(2, dtype=torch.int32, device=self.device)
+        check(lib().moep_input_norm(ptr(x), code, n, self.d, 0, None, None, 0.0, ptr(xb),
+                                    ptr(status), _stream(self.device)), "moep_input_norm")
         st = status.cpu().numpy()
         if st[0]:
             raise ConfigurationError("input must be finite")
         return x, xb, int(st[1]) == 0
+
+    def new_status(self) -> torch.Tensor:
+        """A zeroed K1 status word (int32[1]) for the no-sync serving / bench path."""
+        return torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    @staticmethod
+    def check_status(status: torch.Tensor, x: torch.Tensor) -> None:
+        """Raise the reference's ConfigurationError (predictor.py:188-189) if K1
+        reported non-finite logits and the input itself is non-finite (finite
+        input whose fp32 logits overflowed was recomputed in fp64 and stands).
+        Synchronises on the status word only."""
+        if int(status.max().item()) & 1 and not bool(torch.isfinite(x).all()):
+            raise ConfigurationError("input must be finite")
 
     def normalize(self, x: torch.Tensor, kind: str, gamma=None, beta=None, eps=None) -> torch.Tensor:
         """K0 fused input norm (rmsnorm / layernorm, fp64 stats) -> bf16 x_hat."""
@@ -219,7 +247,7 @@ class DevicePredictor:
         return a
 
     def _k1(self, xb, m_sel=0, bounds=(), ids=None, logits=None, truth=None, k=0, m_values=(),
-            partials=None):
+            partials=None, status=None, kernel=0):
         n = xb.shape[0]
         flags = torch.empty(n, dtype=torch.uint8, device=self.device)
         flag_list = torch.empty(n, dtype=torch.int32, device=self.device)
@@ -233,7 +261,7 @@ class DevicePredictor:
         a.n_bounds = len(bounds)
         for i, b in enumerate(bounds):
             a.bounds[i] = b
-        a.tau_abs, a.tau_rel, a.w2_norm = self.tau_abs, self.tau_rel, self.w2_norm
+        a.tau_abs, a.tau_rel, a.w2_norm = self.tau_abs + self.tau_bias, self.tau_rel, self.w2_norm
         a.ids, a.logits, a.flags = ptr(ids), ptr(logits), ptr(flags)
         a.flag_list, a.flag_count = ptr(flag_list), ptr(flag_count)
         a.truth, a.k, a.n_m = ptr(truth), k, len(m_values)
@@ -244,6 +272,7 @@ class DevicePredictor:
         need = int(lib().moep_predict_split_floats(n, self.hidden, self.E)) if self.split_hidden else 0
         scratch = torch.empty(need, dtype=torch.float32, device=self.device) if need else None
         a.split_scratch, a.split_scratch_floats = ptr(scratch), need
+        a.status, a.kernel = ptr(status), int(kernel)
         check(lib().moep_predict_bf16(a, _stream(self.device)), "moep_predict_bf16")
         return flags, flag_list, flag_count
 
@@ -262,62 +291,93 @@ class DevicePredictor:
         cap = self.fixup_capacity or max(min(n, 64), n // 128)
         return min(cap, n)
 
-    def _fixup(self, a, n, partials2=None):
+    def _fixup(self, a, n, partials2=None, cap=None):
         """Exact fp64 recompute of K1's flagged rows (fast path + overflow)."""
-        cap = self._fixup_cap(n)
+        cap = self._fixup_cap(n) if cap is None else cap
         size = max(cap * ((self.hidden + 127) // 128), min(cap, 1024) * ((self.hidden + 15) // 16)) * self.E
         scratch = torch.empty(size, dtype=torch.float64, device=self.device)
         check(lib().moep_fixup_fp64(a, ptr(scratch), cap, ptr(partials2), _stream(self.device)),
               "moep_fixup_fp64")
 
     # ------------------------------------------------------------------ API
-    def logits(self, x: torch.Tensor, return_flags=False, validate=True):
-        """fp64 logits [N, E] (predict_logits)."""
+    def logits(self, x: torch.Tensor, return_flags=False, validate=True, approx=False):
+        """Logits [N, E] (predict_logits, predictor.py:330-334): exact fp64 for
+        every row (fp64 DMMA GEMM). approx=True: K1's fp32 logits
+        (|dz| <= tau_rel/2 * ||h|| max||w2_e||) with the flagged rows exact."""
         if 0 < x.shape[0] <= self.decode_max_tokens:
             xs, code = self._decode_input(x, validate)
             out64 = torch.empty((xs.shape[0], self.E), dtype=torch.float64, device=self.device)
             self._decode(xs, code, logits64=out64)
             return (out64, None) if return_flags else out64
-        x, xb, exact = self.prepare(x, check_finite=validate)
+        x, xb, exact = self.prepare(x)
         n = x.shape[0]
         out64 = torch.empty((n, self.E), dtype=torch.float64, device=self.device)
-        if self.k1_usable(exact):
+        flags = None
+        if self.k1_usable(exact) and approx:
             lg = torch.empty((n, self.E), dtype=torch.float32, device=self.device)
-            flags, flist, fcount = self._k1(xb, logits=lg)
+            status = self.new_status()
+            flags, flist, fcount = self._k1(xb, logits=lg, status=status)
             out64.copy_(lg)
             a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, logits64=out64)
             self._fixup(a, n)
+            if validate:
+                self.check_status(status, x)
+        elif self.k1_usable(exact):
+            if validate and x.dtype == torch.bfloat16 and not bool(torch.isfinite(x).all()):
+                raise ConfigurationError("input must be finite")
+            self.fp64_rows(xb, out64)
         else:
-            code = MOEP_F64 if x.dtype == torch.float64 else MOEP_BF16
-            xs = x if code == MOEP_F64 or x.dtype == torch.bfloat16 else x.to(torch.float64)
-            code = MOEP_BF16 if xs.dtype == torch.bfloat16 else MOEP_F64
-            a = self._fp64_args(xs, code, logits64=out64)
-            check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
-            flags = None
+            out64 = self.logits_fp64_all(x)
         return (out64, flags) if return_flags else out64
 
-    def topk(self, x: torch.Tensor, m: int, return_flags=False, validate=True):
+    def fp64_rows(self, xb: torch.Tensor, out64: torch.Tensor, row0: int = 0, row1: int | None = None,
+                  chunk: int = 1 << 16) -> torch.Tensor:
+        """Exact fp64 logits of rows [row0, row1) of a bf16 batch into out64 (the
+        fix-up's fp64 DMMA GEMM over a row list, chunked so the per-hidden-tile
+        scratch stays bounded). bf16-exact weights only."""
+        row1 = xb.shape[0] if row1 is None else row1
+        return self.fp64_row_list(xb, torch.arange(row0, row1, dtype=torch.int32, device=self.device), out64,
+                                  chunk)
+
+    def fp64_row_list(self, xb: torch.Tensor, rows: torch.Tensor, out64: torch.Tensor,
+                      chunk: int = 1 << 16) -> torch.Tensor:
+        """Exact fp64 logits of the listed rows (int32, device) into out64[rows]."""
+        rows = rows.to(device=self.device, dtype=torch.int32).contiguous()
+        for s in range(0, rows.shape[0], chunk):
+            r = rows[s: s + chunk]
+            cnt = torch.tensor([r.shape[0]], dtype=torch.int32, device=self.device)
+            a = self._fp64_args(xb, MOEP_BF16, rows=r, row_count=cnt, logits64=out64)
+            self._fixup(a, xb.shape[0], cap=r.shape[0])
+        return out64
+
+    def topk(self, x: torch.Tensor, m: int, return_flags=False, validate=True, status=None):
         """Ascending top-m expert ids [N, m] (predict_topk_batch).
 
         Decode batches (N <= DECODE_MAX_TOKENS) run the exact fp64 decode
         kernel; with validate=False that path does no host synchronisation
-        (serving: the ids feed the prefetch plan on the device)."""
+        (serving: the ids feed the prefetch plan on the device). On the K1
+        path the non-finite-input check reads K1's status word (one host sync
+        when validate; none when the caller passes its own `status`)."""
         if not 1 <= m <= self.E:
             raise ValueError(f"m={m} out of range for {self.E} experts")
         if 0 < x.shape[0] <= self.decode_max_tokens:
-            xs, code = self._decode_input(x, validate)
+            xs, code = self._decode_input(x, validate and status is None)
             ids = torch.empty((xs.shape[0], m), dtype=torch.int32, device=self.device)
             self._decode(xs, code, m_sel=m, ids=ids)
             return (ids, None) if return_flags else ids
-        x, xb, exact = self.prepare(x, check_finite=validate)
+        x, xb, exact = self.prepare(x)
         n = x.shape[0]
         ids = torch.empty((n, m), dtype=torch.int32, device=self.device)
         flags = None
         if self.k1_usable(exact, (m,)):
+            own = status is None
+            st = self.new_status() if own else status
             bounds = (m,) if m < self.E else ()
-            flags, flist, fcount = self._k1(xb, m_sel=m, bounds=bounds, ids=ids)
+            flags, flist, fcount = self._k1(xb, m_sel=m, bounds=bounds, ids=ids, status=st)
             a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, m_sel=m, ids=ids)
             self._fixup(a, n)
+            if own and validate:
+                self.check_status(st, x)
         else:
             xs = x if x.dtype in (torch.float64, torch.bfloat16) else x.to(torch.float64)
             code = MOEP_BF16 if xs.dtype == torch.bfloat16 else MOEP_F64
@@ -326,23 +386,26 @@ class DevicePredictor:
         return (ids, flags) if return_flags else ids
 
     def evaluate(self, x: torch.Tensor, truth: torch.Tensor, k: int, m_values, ids_m: int = 0,
-                 prepared=None, k1_events=None) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
-        """Fused predict + evaluation counters on device.
+                 k1_events=None, status=None, validate=True) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+        """Fused predict + evaluation counters on device (metrics.py:138-207).
 
+        status: the caller's K1 status word (int32[1], zeroed; see new_status /
+        check_status): nothing synchronises and the caller checks it when it
+        reads the counters. Without it, validate=True checks it here (one host
+        sync on a 4-byte word; no extra pass over x).
         k1_events: optional (start, end) CUDA events recorded on the current
         stream around the fused tensor-core kernel alone (profiling hook).
 
-        Returns (counters int64 [n_counters], flag_count int32 [1], ids or None)
-        without synchronising; see EvalCounters.from_array for the layout.
+        Returns (counters int64 [n_counters], flag_count int32 [1], ids or None);
+        see EvalCounters.from_array for the layout.
         """
         m_values = sorted(set(int(m) for m in m_values))
         if k not in m_values:
             m_values.insert(0, k)
         truth = truth.to(device=self.device, dtype=torch.int32).contiguous()
         ncnt = 2 + 2 * len(m_values) + 2 * self.E
-        if prepared is None and 0 < x.shape[0] <= self.decode_max_tokens and len(m_values) <= _lib.MAX_BOUNDS \
-                and k <= 16:
-            xs, code = self._decode_input(x, True)
+        if 0 < x.shape[0] <= self.decode_max_tokens and len(m_values) <= _lib.MAX_BOUNDS and k <= 16:
+            xs, code = self._decode_input(x, validate and status is None)
             partials = torch.empty((self.n_sms, ncnt), dtype=torch.int32, device=self.device)
             counters = torch.empty(ncnt, dtype=torch.int64, device=self.device)
             ids = torch.empty((xs.shape[0], ids_m), dtype=torch.int32, device=self.device) if ids_m else None
@@ -350,10 +413,7 @@ class DevicePredictor:
             check(lib().moep_counters_reduce(ptr(partials), self.n_sms, ncnt, ptr(counters),
                                              _stream(self.device)), "moep_counters_reduce")
             return counters, torch.zeros(1, dtype=torch.int32, device=self.device), ids
-        if prepared is None:
-            x, xb, exact = self.prepare(x)
-        else:
-            x, xb, exact = prepared
+        x, xb, exact = self.prepare(x)
         n = x.shape[0]
         # partial rows: [K1 | fix-up finish | fix-up overflow], one per SM each
         partials = torch.empty((3 * self.n_sms, ncnt), dtype=torch.int32, device=self.device)
@@ -363,10 +423,12 @@ class DevicePredictor:
         bounds = tuple(p for p in positions if p < self.E)
         if len(m_values) <= _lib.MAX_BOUNDS and len(bounds) <= _lib.MAX_BOUNDS and self.k1_usable(exact, bounds) \
                 and k <= 16:
+            own = status is None
+            st = self.new_status() if own else status
             if k1_events is not None:
                 k1_events[0].record()
             flags, flist, fcount = self._k1(xb, m_sel=ids_m, bounds=bounds, ids=ids, truth=truth, k=k,
-                                            m_values=m_values, partials=partials[: self.n_sms])
+                                            m_values=m_values, partials=partials[: self.n_sms], status=st)
             if k1_events is not None:
                 k1_events[1].record()
             a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, m_sel=ids_m, ids=ids,
@@ -376,9 +438,13 @@ class DevicePredictor:
             nrow = 3 if self._fixup_cap(n) < n else 2  # overflow partials only when they can exist
             check(lib().moep_counters_reduce(ptr(partials), nrow * self.n_sms, ncnt, ptr(counters),
                                              _stream(self.device)), "moep_counters_reduce")
+            if own and validate:
+                self.check_status(st, x)
             return counters, fcount, ids
         # general path: exact fp64 logits for every token, then K7 from logits
         z = self.logits_fp64_all(x)
+        if validate and not bool(torch.isfinite(z).all()) and not bool(torch.isfinite(x).all()):
+            raise ConfigurationError("input must be finite")
         counters = eval_logits_device(z, truth, k, self.E, m_values)
         if ids_m:
             ids = topk_logits_device(z, ids_m)

@@ -62,15 +62,17 @@ def test_struct_layouts_match_header(libpath):
     src = f'''#include "{HEADER}"
 #include <stdio.h>
 #include <stddef.h>
-int main(){{printf("%zu %zu %zu %zu\\n", sizeof(moep_predict_args), offsetof(moep_predict_args, partials),
- sizeof(moep_fp64_args), offsetof(moep_fp64_args, partials));return 0;}}'''
+int main(){{printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(moep_predict_args), offsetof(moep_predict_args, partials),
+ sizeof(moep_fp64_args), offsetof(moep_fp64_args, partials), offsetof(moep_predict_args, status),
+ offsetof(moep_predict_args, kernel));return 0;}}'''
     tmp = "/tmp/moep_layout_probe"
     with open(tmp + ".c", "w") as f:
         f.write(src)
     subprocess.run(["gcc", "-o", tmp, tmp + ".c"], check=True)
     got = [int(v) for v in subprocess.run([tmp], capture_output=True, text=True).stdout.split()]
     assert got == [ctypes.sizeof(_lib.PredictArgs), _lib.PredictArgs.partials.offset,
-                   ctypes.sizeof(_lib.Fp64Args), _lib.Fp64Args.partials.offset]
+                   ctypes.sizeof(_lib.Fp64Args), _lib.Fp64Args.partials.offset,
+                   _lib.PredictArgs.status.offset, _lib.PredictArgs.kernel.offset]
 
 
 def test_loss_and_optim_struct_layouts(libpath):

@@ -1,7 +1,8 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
-reference's golden fixtures. Bit-exact for ids / counters; logits within the
-stated tolerance (1e-5 absolute for the bf16 tensor-core path before fix-up,
-exact-fp64 rows after)."""
+reference's golden fixtures. Bit-exact for ids / counters; predict_logits is
+exact fp64 (fixed summation order, so within 1e-11 of numpy's BLAS order);
+K1's raw fp32 logits (logits(approx=True)) within tau_rel/2 of the row scale
+||h|| max_e||w2_e||, the margin contract of DESIGN §3."""
 
 import numpy as np
 import pytest
@@ -10,7 +11,7 @@ torch = pytest.importorskip("torch")
 
 pytestmark = pytest.mark.gpu
 
-LOGIT_ATOL_K1 = 2e-5  # raw K1 logits vs fp64 (tensor-core fp32 accumulation, truncating)
+LOGIT_ATOL = 1e-11   # predict_logits (exact fp64, fixed order) vs numpy fp64 (BLAS order)
 
 
 @pytest.fixture(scope="module")
@@ -67,7 +68,7 @@ def test_c1_golden_ids(pb, golden, O):
     assert np.array_equal(pb.predict_topk_batch(m, x, 6), g["c1_top6"])
     assert np.array_equal(pb.predict_topk_batch(m, x, 10), g["c1_top10"])
     z = pb.predict_logits(m, x)
-    assert np.abs(z - g["c1_logits"]).max() < LOGIT_ATOL_K1
+    assert np.abs(z - g["c1_logits"]).max() < LOGIT_ATOL
 
 
 def test_topk_golden(pb, golden):
@@ -141,7 +142,7 @@ def test_k1_ids_and_counters_vs_oracle(pb, O, arch, d, h, e, k, n):
             ids, flags = dev.topk(xt, mm, return_flags=True)
             assert np.array_equal(ids.cpu().numpy(), O.top_k_batch(zref, mm)), mm
     z = dev.logits(xt).cpu().numpy()
-    assert np.abs(z - zref).max() < LOGIT_ATOL_K1
+    assert np.abs(z - zref).max() < LOGIT_ATOL
     truth = O.top_k_batch(zref + 0.05 * rng.standard_normal(zref.shape), k)  # correlated truth
     ms = O.default_m_list(k, e)
     cnt, fcount, _ = dev.evaluate(xt, torch.from_numpy(truth), k, ms)
@@ -153,22 +154,30 @@ def test_k1_ids_and_counters_vs_oracle(pb, O, arch, d, h, e, k, n):
     assert np.array_equal(c.per_expert_truth, oc["per_expert_truth"])
 
 
-def test_margin_covers_error(pb, O):
-    """Calibration guard: raw K1 error / row scale stays well inside tau_rel."""
+@pytest.mark.parametrize("n,e,kernel", [(16384, 64, 2), (40000, 64, 4), (65536, 128, 4), (40000, 16, 4),
+                                        (4096, 32, 1)])
+def test_margin_covers_error(pb, O, n, e, kernel):
+    """Calibration guard: K1's raw error / row scale stays 8x inside the margin
+    (max <= tau/8; tau/2 is the hard limit) on each kernel: v2 (one wave), v4
+    (>= 2 tiles per CTA pair; E = 128 has no separate lo accumulator and runs
+    with 1.5 tau) and the 1-SM kernel."""
+    from paper_2511_10676_b200 import _lib
     from paper_2511_10676_b200.engine import TAU_REL
-    rng = np.random.default_rng(11)
-    n, d, h, e = 16384, 2048, 2048, 64
+    rng = np.random.default_rng(11 + e)
+    d = h = 2048 if kernel != 1 else 512
+    if kernel == 1:
+        h = 384
     m = bf16_model(pb, O, "arch2", d, h, e, seed=5)
     x = O.round_bf16(rng.standard_normal((n, d)))
     zref, cache = O.forward_eval(oracle_params(m), x)
     dev = m.to_device()
     lg = torch.empty((n, e), dtype=torch.float32, device="cuda")
-    dev._k1(torch.from_numpy(x).to("cuda", torch.bfloat16), logits=lg)
+    dev._k1(torch.from_numpy(x).to("cuda", torch.bfloat16), logits=lg, kernel=kernel)
     err = np.abs(lg.double().cpu().numpy() - zref).max(axis=1)
     scale = np.linalg.norm(cache["h"], axis=1) * np.linalg.norm(m.w2, axis=1).max()
     ratio = err / scale
-    # a decision flips only if two errors add up to delta: require 2*max < tau
-    assert 2 * ratio.max() < TAU_REL, ratio.max()
+    tau = TAU_REL * (1.5 if (kernel == 4 and e > 64) or kernel == 1 else 1.0)
+    assert 8 * ratio.max() <= tau, (ratio.max(), tau)
 
 
 @pytest.mark.parametrize("n,e", [(256, 64), (4096, 64), (8192, 128), (300, 16)])
@@ -190,7 +199,7 @@ def test_margin_covers_error_hidden_split(pb, O, n, e):
     dev._k1(xt, logits=lg)
     err = np.abs(lg.double().cpu().numpy() - zref).max(axis=1)
     scale = np.linalg.norm(cache["h"], axis=1) * np.linalg.norm(m.w2, axis=1).max()
-    assert 2 * (err / scale).max() < TAU_REL, (err / scale).max()
+    assert 8 * (err / scale).max() <= TAU_REL, (err / scale).max()
     dev.decode_max_tokens = 0
     ids_split = dev.topk(xt, 6).cpu().numpy()
     dev.split_hidden = False
@@ -247,6 +256,98 @@ def test_nonfinite_input_raises(pb, O):
         pb.predict_logits(m, x)
     with pytest.raises(pb.ConfigurationError):
         pb.predict_logits(m, np.zeros((4, 65)))
+
+
+@pytest.mark.parametrize("n", [3000, 40000])
+def test_nonfinite_bf16_input_raises_through_k1_status(pb, O, n):
+    """bf16 device input takes K1 with no isfinite pass: a NaN / Inf token makes
+    its fp32 logits non-finite, K1 sets its status word and the API raises the
+    reference's ConfigurationError (predictor.py:188-189). With the caller's own
+    status word nothing synchronises; check_status raises afterwards."""
+    rng = np.random.default_rng(4)
+    m = bf16_model(pb, O, "arch2", 512, 512, 64, seed=1)
+    dev = m.to_device()
+    dev.decode_max_tokens = 0
+    x = torch.from_numpy(O.round_bf16(rng.standard_normal((n, 512)))).to("cuda", torch.bfloat16)
+    truth = torch.from_numpy(O.top_k_batch(rng.standard_normal((n, 64)), 6))
+    st = dev.new_status()
+    dev.topk(x, 6, status=st)
+    dev.evaluate(x, truth, 6, [6, 10, 64], ids_m=6, status=st)
+    assert int(st.item()) == 0
+    dev.check_status(st, x)
+    for bad in (float("nan"), float("inf")):
+        xb = x.clone()
+        xb[n // 2, 7] = bad
+        with pytest.raises(pb.ConfigurationError):
+            dev.topk(xb, 6)
+        with pytest.raises(pb.ConfigurationError):
+            dev.evaluate(xb, truth, 6, [6, 10, 64])
+        st = dev.new_status()
+        dev.evaluate(xb, truth, 6, [6, 10, 64], ids_m=6, status=st)
+        assert int(st.item()) & 1
+        with pytest.raises(pb.ConfigurationError):
+            dev.check_status(st, xb)
+
+
+def test_large_biases_in_margin(pb, O):
+    """Biases far above the logit scale: K1 holds b1 / b2 in fp32,
+    so the margin adds 2^-21 (max|b2| + 1.2 max||w2_e|| ||b1||); ids and
+    counters must still equal the oracle's."""
+    rng = np.random.default_rng(31)
+    n, d, h, e, k = 40000, 2048, 2048, 64, 6
+    m = bf16_model(pb, O, "arch2", d, h, e, seed=8)
+    m.b2 = 200.0 + 0.02 * rng.standard_normal(e)   # logits ~ N(0, 0.18) on top of ~200
+    m.b1 = 3.0 * rng.standard_normal(h)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref = O.predict_logits(oracle_params(m), x)
+    dev = m.to_device()
+    assert dev.tau_bias > 0
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    for mm in (1, 6, 10):
+        assert np.array_equal(dev.topk(xt, mm).cpu().numpy(), O.top_k_batch(zref, mm)), mm
+    truth = O.top_k_batch(zref + 0.05 * rng.standard_normal(zref.shape), k)
+    cnt, _, ids = dev.evaluate(xt, torch.from_numpy(truth), k, [6, 10, 64], ids_m=6)
+    c = pb.EvalCounters.from_array(cnt.cpu().numpy(), k, e, [6, 10, 64])
+    oc = O.eval_counters(zref, truth, e, [6, 10, 64])
+    assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"] and c.top1 == oc["top1_count"]
+    assert np.array_equal(ids.cpu().numpy(), O.top_k_batch(zref, 6))
+
+
+def test_forced_kernels_agree(pb, O):
+    """The three K1 kernels (1-SM, pair v2, pair v4; moep_predict_args.kernel)
+    give identical ids on the same input after the fix-up."""
+    rng = np.random.default_rng(12)
+    n, d, h, e = 40000, 1024, 1024, 64
+    m = bf16_model(pb, O, "arch2", d, h, e, seed=12)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref = O.predict_logits(oracle_params(m), x)
+    ref = O.top_k_batch(zref, 6)
+    dev = m.to_device()
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    from paper_2511_10676_b200.engine import MOEP_BF16
+    for kern in (1, 2, 4):
+        ids = torch.empty((n, 6), dtype=torch.int32, device="cuda")
+        flags, flist, fcount = dev._k1(xt, m_sel=6, bounds=(6,), ids=ids, kernel=kern)
+        a = dev._fp64_args(xt, MOEP_BF16, rows=flist, row_count=fcount, m_sel=6, ids=ids)
+        dev._fixup(a, n)
+        assert np.array_equal(ids.cpu().numpy(), ref), kern
+
+
+def test_logits_exact_and_approx(pb, O):
+    """predict_logits returns exact fp64 for every row; the opt-in
+    approx=True returns K1's fp32 logits, each within tau/2 of the row scale."""
+    rng = np.random.default_rng(19)
+    n, d, h, e = 5000, 2048, 2048, 64
+    m = bf16_model(pb, O, "arch2", d, h, e, seed=2)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref, cache = O.forward_eval(oracle_params(m), x)
+    dev = m.to_device()
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    assert np.allclose(dev.logits(xt).cpu().numpy(), zref, rtol=0, atol=LOGIT_ATOL)
+    assert np.allclose(pb.predict_logits(m, x), zref, rtol=0, atol=LOGIT_ATOL)
+    za = dev.logits(xt, approx=True).cpu().numpy()
+    scale = np.linalg.norm(cache["h"], axis=1) * np.linalg.norm(m.w2, axis=1).max()
+    assert (np.abs(za - zref).max(axis=1) <= dev.tau_rel / 2 * scale + dev.tau_abs).all()
 
 
 def test_single_vector_and_m_range(pb, O):
@@ -311,7 +412,7 @@ def test_fixup_overflow_path(pb, O, tau_rel, lo, hi):
         assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
         assert c.top1 == oc["top1_count"] and np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
         z = dev.logits(xt).cpu().numpy()
-        assert np.abs(z - zref).max() < LOGIT_ATOL_K1
+        assert np.abs(z - zref).max() < LOGIT_ATOL
 
 
 # ------------------------------------------------ shape / argument edge cases

@@ -14,11 +14,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_10676_b200 as pb  # noqa: E402
 from oracle import oracle as O  # noqa: E402  (measurement tool: the oracle is the checker)
 
+import workloads as W  # noqa: E402
+
 n, d, h, e = 16384, 2048, 2048, 64
-rng = np.random.default_rng(11)
-m = pb.init_model("arch2", d, h, e, seed=5)
-m.w1, m.w2 = O.round_bf16(m.w1), O.round_bf16(m.w2)
-x = O.round_bf16(rng.standard_normal((n, d)))
+KIND = sys.argv[1] if len(sys.argv) > 1 else "random"
+m, xt0, _ = W.make_layer(KIND, d, h, e, 6, n, seed=5, device="cuda")
+x = xt0.double().cpu().numpy()
+print("workload", KIND)
 p = {"arch": "arch2", "w1": m.w1, "b1": m.b1, "w2": m.w2, "b2": m.b2}
 zref, cache = O.forward_eval(p, x)
 dev = m.to_device()

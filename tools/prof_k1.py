@@ -11,6 +11,6 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
 layers = bench.make_layers(torch.device("cuda"), 1, n, 0)
 model, dp, x, truth = layers[0]
 for _ in range(3):
-    cnt, fc, _ = dp.evaluate(x, truth, 6, [6, 10, 64], prepared=(x, x, True))
+    cnt, fc, _ = dp.evaluate(x, truth, 6, [6, 10, 64], ids_m=6)
 torch.cuda.synchronize()
 print("flagged", int(fc.item()), "k1 ms", bench.time_k1(dp, x, truth, reps=3))
