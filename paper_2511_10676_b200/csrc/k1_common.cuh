@@ -132,9 +132,34 @@ __device__ __forceinline__ void row_epilogue_core(const Params& p, ZGet zv, bool
           if ((p.ids && pos == p.m_sel) || !eval_only_ok) {
             flagged = true;
           } else {
+            // only experts inside the window can cross this boundary. At pos == k
+            // per_expert_hits names the true experts inside the top-k: any true
+            // expert in the window counts. At the other positions (1: top1;
+            // m: overprov / recall) only the NUMBER of true experts above the
+            // boundary counts, which cannot change when the window holds true
+            // experts only (or none)
+            const float wlo = lo_v - delta, whi = hi_v + delta;
+            int nt = 0;
             for (int j = 0; j < p.k; ++j) {
               const float zt = zrow[__ldg(p.truth + row * p.k + j) ^ zswz];
-              flagged |= !(zt <= lo_v - delta || zt >= hi_v + delta);
+              nt += !(zt <= wlo || zt >= whi) ? 1 : 0;
+            }
+            if (pos == p.k) {
+              flagged |= nt > 0;
+            } else if (nt > 0) {
+              // window experts, and how many of them are true (distinct ids:
+              // a repeated true id must not mask a non-true expert)
+              int nw = 0, ntw = 0;
+              for (int e = 0; e < p.E; ++e) {
+                const float v = zrow[e ^ zswz];  // the staged copy (written whenever truth is given)
+                if (!(v <= wlo || v >= whi)) {
+                  ++nw;
+                  bool is_t = false;
+                  for (int j = 0; j < p.k; ++j) is_t |= __ldg(p.truth + row * p.k + j) == e;
+                  ntw += is_t ? 1 : 0;
+                }
+              }
+              flagged |= nw > ntw;
             }
           }
         }

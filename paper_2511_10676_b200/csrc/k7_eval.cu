@@ -168,14 +168,11 @@ eval_reg_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict
 #pragma unroll
       for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi)
         inside[mi] = __popc(__ballot_sync(0xffffffffu, mine && my_rank < m_of[mi]) & submask);
-      // true ids of a token are distinct: lanes j < k of a token update
-      // different bins; the tokens of a warp use their own hist copies in turn
-      for (int g = 0; g < RPW; ++g) {
-        if (sub == g && ok && li < k) {
-          hist[E + tv[r]] += 1;
-          if (my_rank < k) hist[tv[r]] += 1;
-        }
-        __syncwarp();
+      // shared atomics: a token's true ids may repeat (the reference's
+      // bincount counts every occurrence, metrics.py:182-187)
+      if (ok && li < k) {
+        atomicAdd(&hist[E + tv[r]], 1);
+        if (my_rank < k) atomicAdd(&hist[tv[r]], 1);
       }
       if (ok && li == 0) {
         cnt[0] += 1;

@@ -146,7 +146,7 @@ def loss_and_grad(spec: LossSpec, logits, labels: BatchLabels):
     z = _check_shape(logits, labels)
     dt = z.dtype if (is_t and z.dtype in (torch.float32, torch.float64)) else torch.float64
     z = z.to("cuda", dt).contiguous()
-    scores, mask, rank = labels.to_device(dt)
+    scores, mask, rank = BatchLabels.to_device(labels, dt)  # any object with the three fields (the reference's too)
     out, dz = device_loss(spec, z, scores, mask, rank)
     loss = float(out[0].item())
     return (loss, dz) if is_t else (loss, dz.cpu().numpy())
@@ -175,7 +175,7 @@ def ranking_hinge(logits, labels: BatchLabels, *, margin=0.1, normalize=True):
     K4 family code 4 = hinge term only (lambda 1, no WBCE part)."""
     is_t = isinstance(logits, torch.Tensor)
     z = _check_shape(logits, labels).to("cuda", torch.float64).contiguous()
-    scores, mask, rank = labels.to_device(torch.float64)
+    scores, mask, rank = BatchLabels.to_device(labels, torch.float64)
     spec = LossSpec("ranking", ranking_lambda=1.0, margin=margin, normalize_ranking=normalize)
     out, dz = device_loss(spec, z, scores, mask, rank, family_code=4)
     o = out.cpu().numpy()
@@ -187,7 +187,7 @@ def mse_loss(pred_scores, labels: BatchLabels):
     Small helper on device tensors (not on the training hot path)."""
     is_t = isinstance(pred_scores, torch.Tensor)
     p = _check_shape(pred_scores, labels).to("cuda", torch.float64)
-    s, _, _ = labels.to_device(torch.float64)
+    s, _, _ = BatchLabels.to_device(labels, torch.float64)
     n = p.shape[0]
     diff = s - p
     loss = float((diff * diff).sum().item() / n)

@@ -134,10 +134,58 @@ def _as_batch(model: PredictorModel, x):
     return torch.from_numpy(np.ascontiguousarray(batch)), single, False
 
 
+_DEV_CACHE: "dict[int, tuple]" = {}
+_DEV_CACHE_MAX = 8
+_SAMPLE = 4096
+
+
+def _fingerprint(model) -> tuple:
+    """Identity, buffer address, shape and a strided 4096-element sample of
+    every parameter / BN array: an in-place update of the weights (the
+    reference's optimizer, trainer.py:91-122, rewrites every element) or a new
+    array changes it; a forced refresh is `device_for(model, refresh=True)`."""
+    fp = [model.arch]
+    for name in ("w1", "b1", "w2", "b2", "bn_scale", "bn_shift", "bn_mean", "bn_var"):
+        a = getattr(model, name, None)
+        if a is None:
+            fp.append(None)
+            continue
+        a = np.asarray(a)
+        flat = a.reshape(-1)
+        step = max(1, flat.size // _SAMPLE)
+        fp.append((id(a), a.__array_interface__["data"][0], a.shape, a.dtype.str,
+                   flat[::step][:_SAMPLE].tobytes(), flat[-1:].tobytes()))
+    return tuple(fp)
+
+
+def device_for(model, refresh: bool = False) -> DevicePredictor:
+    """The HBM-resident DevicePredictor of a host model, uploaded once and
+    reused while the model's parameters are unchanged (the reference API
+    functions take host models; re-uploading 33.5 MB of fp64 W1 per call cost
+    ~8x a 4k-token predict). Keyed by id(model) + _fingerprint; a small LRU."""
+    key = id(model)
+    fp = _fingerprint(model)
+    hit = _DEV_CACHE.get(key)
+    if hit is not None and not refresh and hit[0] == fp and hit[2]() is model:
+        _DEV_CACHE[key] = _DEV_CACHE.pop(key)  # most recent last
+        return hit[1]
+    import weakref
+    dev = DevicePredictor(model)
+    try:
+        ref = weakref.ref(model)
+    except TypeError:  # an object without weakref support: keep it alive with the entry
+        ref = (lambda m: (lambda: m))(model)
+    _DEV_CACHE.pop(key, None)
+    _DEV_CACHE[key] = (fp, dev, ref)
+    while len(_DEV_CACHE) > _DEV_CACHE_MAX:
+        _DEV_CACHE.pop(next(iter(_DEV_CACHE)))
+    return dev
+
+
 def predict_logits(model: PredictorModel, x):
     """Eval-mode logits regardless of the mode flag (predictor.py:330-334)."""
     batch, single, is_t = _as_batch(model, x)
-    z = DevicePredictor(model).logits(batch.to("cuda"))
+    z = device_for(model).logits(batch.to("cuda"))
     if not is_t:
         z = z.cpu().numpy()
     return z[0] if single else z
@@ -148,7 +196,7 @@ def predict_topk_batch(model: PredictorModel, x, m: int):
     if not 1 <= m <= model.n_experts:
         raise ValueError(f"m={m} out of range for {model.n_experts} experts")
     batch, single, is_t = _as_batch(model, x)
-    ids = DevicePredictor(model).topk(batch.to("cuda"), m).to(torch.int64)
+    ids = device_for(model).topk(batch.to("cuda"), m).to(torch.int64)
     return ids if is_t else ids.cpu().numpy()
 
 
@@ -159,7 +207,7 @@ def predict_topk(model: PredictorModel, x, m: int) -> ExpertSelection:
     if not 1 <= m <= model.n_experts:
         raise ValueError(f"m={m} out of range for {model.n_experts} experts")
     x = np.asarray(x, dtype=np.float64).reshape(-1)
-    dev = DevicePredictor(model)
+    dev = device_for(model)
     batch = torch.from_numpy(x[None, :]).to("cuda")
     logits = dev.logits(batch)[0].cpu().numpy()
     ids = dev.topk(batch, m)[0].cpu().numpy()

@@ -222,7 +222,14 @@ class DeviceTrainer:
         check(lib().moep_optim_step(A, _stream(self.dev)), "moep_optim_step")
 
     def step(self, x, scores, mask, rank, n_global=None):
-        """One training step; returns the device loss tensor [loss, n_pairs] (no host sync)."""
+        """One training step; returns the device loss tensor [loss, n_pairs] (no host sync).
+
+        Under data parallelism a rank whose slice of the minibatch is empty
+        (a last minibatch smaller than the world) still joins both all-reduces
+        with zero partial sums and a zero gradient, so its peers do not wait
+        forever and every rank applies the same update."""
+        if x.shape[0] == 0:
+            return self._empty_step(n_global or 0)
         z, cache, x_used = self.forward(x)
         zs = z if scores.dtype == z.dtype else z.to(scores.dtype)
         out, dz = device_loss(self.loss_spec, zs, scores, mask, rank, n_global=n_global,
@@ -230,6 +237,22 @@ class DeviceTrainer:
         if dz.dtype != self.dt:
             dz = dz.to(self.dt)
         self.backward(x_used, cache, dz.contiguous())
+        if self.grad_allreduce is not None:
+            self.grad_allreduce(self.grad)
+        self.optimizer_step()
+        return out
+
+    def _empty_step(self, n_global):
+        from .losses import FAMILY_CODE
+        code = FAMILY_CODE[self.loss_spec.family]
+        partials = torch.zeros((1, 3), dtype=torch.float64, device=self.dev)
+        if self.loss_allreduce is not None:
+            self.loss_allreduce(partials)
+        out = torch.empty(2, dtype=torch.float64, device=self.dev)
+        check(lib().moep_loss_finalize(ptr(partials), 1, 0, self.E, code, self.loss_spec.ranking_lambda,
+                                       int(self.loss_spec.normalize_ranking), dtype_code(self.flat), None, None,
+                                       ptr(out), _stream(self.dev)), "moep_loss_finalize")
+        self.grad.zero_()
         if self.grad_allreduce is not None:
             self.grad_allreduce(self.grad)
         self.optimizer_step()
