@@ -172,12 +172,20 @@ int moep_counters_reduce(const int32_t* partials, int32_t n_blocks, int32_t n_co
                          int64_t* out, void* stream);
 
 /* ------------------------------------------------------------------ K0 --
- * Pre-attention input norm: fp64 statistics, output rounded fp64 -> bf16 RNE.
+ * Pre-attention input norm at the hook point (hooks.py:19,113-114; the
+ * reference's norm is core.layer_norm, core.py:57-68), output rounded fp64 ->
+ * bf16 RNE, bit-identical to numpy by construction: the statistics follow
+ * numpy's pairwise reduction order and every element's bf16 rounding equals
+ * that of numpy's (x - mean) / sqrt(var + eps) [* gamma] [+ beta] chain
+ * (k0_norm.cu: a reciprocal multiply, with the exact chain for values near a
+ * bf16 rounding midpoint).
  * kind: 0 none (cast), 1 rmsnorm(gamma, eps), 2 layernorm(gamma, beta, eps).
- * x dtype: MOEP_BF16, MOEP_F32 or MOEP_F64. Also reports non-finite input
- * through status[0] (ConfigurationError contract of predictor.py:188-189) and,
- * for kind 0, counts rows holding values that are not bf16-representable in
- * status[1] (those inputs take the fp64 path). status is int32[2], caller-zeroed. */
+ * x dtype: MOEP_BF16, MOEP_F32 or MOEP_F64. bf16 rows with d in {512, 1024,
+ * 2048, 4096} take the one-pass HBM-rate kernel; other shapes a general
+ * kernel. Also reports non-finite input rows through status[0]
+ * (ConfigurationError contract of predictor.py:188-189) and, for kind 0,
+ * counts values that are not bf16-representable in status[1] (those inputs
+ * take the fp64 path). status is int32[2], caller-zeroed. */
 int moep_input_norm(const void* x, int32_t x_dtype, int64_t n, int32_t d, int32_t kind,
                     const double* gamma, const double* beta, double eps, void* xhat_bf16,
                     int32_t* status, void* stream);

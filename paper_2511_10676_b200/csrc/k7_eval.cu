@@ -341,78 +341,6 @@ __global__ void __launch_bounds__(1024) reduce_kernel(const int* __restrict__ pa
 }
 
 // ------------------------------------------------------------- K0: input norm
-template <int XT>
-__device__ __forceinline__ double ldx(const void* p, int64_t i) {
-  if (XT == MOEP_BF16) return static_cast<double>(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]));
-  if (XT == MOEP_F32) return static_cast<double>(reinterpret_cast<const float*>(p)[i]);
-  return reinterpret_cast<const double*>(p)[i];
-}
-
-__device__ double block_sum(double v, double* red) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < NT / 32; ++w) t += red[w];
-  return t;
-}
-
-template <int XT>
-__global__ void __launch_bounds__(NT)
-norm_kernel(const void* x, int64_t n, int d, int kind, const double* gamma, const double* beta,
-            double eps, __nv_bfloat16* out, int* status) {
-  __shared__ double red[NT / 32];
-  for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
-    int bad = 0, inexact = 0;
-    double mu = 0.0, scale = 1.0;
-    if (kind != 0) {
-      double s = 0.0, s2 = 0.0;
-      for (int i = threadIdx.x; i < d; i += NT) {
-        const double v = ldx<XT>(x, row * d + i);
-        bad |= !isfinite(v);
-        s += v;
-        s2 += v * v;
-      }
-      const double sum = block_sum(s, red);
-      if (kind == 1) {
-        const double ms = block_sum(s2, red) / d;
-        scale = sqrt(ms + eps);
-      } else {
-        mu = sum / d;
-        double sv = 0.0;
-        for (int i = threadIdx.x; i < d; i += NT) {
-          const double c = ldx<XT>(x, row * d + i) - mu;
-          sv += c * c;
-        }
-        scale = sqrt(block_sum(sv, red) / d + eps);
-      }
-    }
-    for (int i = threadIdx.x; i < d; i += NT) {
-      const double v = ldx<XT>(x, row * d + i);
-      double y;
-      if (kind == 0) {
-        y = v;
-        bad |= !isfinite(v);
-      } else if (kind == 1) {
-        y = v / scale;
-        if (gamma) y = y * gamma[i];
-      } else {
-        y = (v - mu) / scale;
-        if (gamma) y = y * gamma[i];
-        if (beta) y = y + beta[i];
-      }
-      const __nv_bfloat16 b = f64_to_bf16_rne(y);
-      if (kind == 0) inexact |= static_cast<double>(__bfloat162float(b)) != y;
-      out[row * d + i] = b;
-    }
-    if (bad) atomicAdd(status, 1);
-    if (inexact) atomicAdd(status + 1, 1);
-  }
-}
-
 }  // namespace k7
 }  // namespace moep
 
@@ -537,22 +465,6 @@ int moep_counters_reduce(const int32_t* partials, int32_t n_blocks, int32_t n_co
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   moep::k7::reduce_kernel<<<(n_counters + 31) / 32, 1024, 0, st>>>(
       partials, n_blocks, n_counters, reinterpret_cast<long long*>(out));
-  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
-}
-
-int moep_input_norm(const void* x, int32_t x_dtype, int64_t n, int32_t d, int32_t kind,
-                    const double* gamma, const double* beta, double eps, void* xhat_bf16,
-                    int32_t* status, void* stream) {
-  using namespace moep::k7;
-  if (n <= 0 || d <= 0) return MOEP_ESHAPE;
-  if (kind < 0 || kind > 2 || !status) return MOEP_EARG;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int grid = static_cast<int>(n < 65536 ? n : 65536);
-  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(xhat_bf16);
-  if (x_dtype == MOEP_BF16) norm_kernel<MOEP_BF16><<<grid, NT, 0, st>>>(x, n, d, kind, gamma, beta, eps, out, status);
-  else if (x_dtype == MOEP_F32) norm_kernel<MOEP_F32><<<grid, NT, 0, st>>>(x, n, d, kind, gamma, beta, eps, out, status);
-  else if (x_dtype == MOEP_F64) norm_kernel<MOEP_F64><<<grid, NT, 0, st>>>(x, n, d, kind, gamma, beta, eps, out, status);
-  else return MOEP_EARG;
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }
 

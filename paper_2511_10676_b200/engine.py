@@ -185,22 +185,13 @@ class DevicePredictor:
         if int(status.max().item()) & 1 and not bool(torch.isfinite(x).all()):
             raise ConfigurationError("input must be finite")
 
-    def normalize(self, x: torch.Tensor, kind: str, gamma=None, beta=None, eps=None) -> torch.Tensor:
-        """K0 fused input norm (rmsnorm / layernorm, fp64 stats) -> bf16 x_hat."""
-        kinds = {"none": 0, "rmsnorm": 1, "layernorm": 2}
-        if kind not in kinds:
-            raise ConfigurationError(f"unknown norm kind {kind!r}")
-        eps = (1e-6 if kind == "rmsnorm" else 1e-5) if eps is None else eps
-        x = x.to(self.device).contiguous()
-        code = {torch.bfloat16: MOEP_BF16, torch.float64: MOEP_F64, torch.float32: _lib.MOEP_F32}[x.dtype]
-        out = torch.empty(x.shape, dtype=torch.bfloat16, device=self.device)
-        status = torch.zeros(2, dtype=torch.int32, device=self.device)
-        g = None if gamma is None else torch.as_tensor(gamma, dtype=torch.float64, device=self.device)
-        b = None if beta is None else torch.as_tensor(beta, dtype=torch.float64, device=self.device)
-        check(lib().moep_input_norm(ptr(x), code, x.shape[0], x.shape[1], kinds[kind], ptr(g), ptr(b),
-                                    float(eps), ptr(out), ptr(status), _stream(self.device)),
-              "moep_input_norm")
-        return out
+    def normalize(self, x: torch.Tensor, kind: str, gamma=None, beta=None, eps=None, status=None,
+                  _force_exact=False) -> torch.Tensor:
+        """K0 input norm at the hook point (rmsnorm / layernorm with fp64
+        statistics in numpy's order) -> bf16 x_hat, bit-identical to
+        oracle.input_norm_bf16. Non-finite rows raise ConfigurationError (one
+        host sync) unless the caller passes its own int32[2] `status`."""
+        return input_norm(x, kind, gamma, beta, eps, status=status, device=self.device, _force_exact=_force_exact)
 
     def _decode_input(self, x: torch.Tensor, validate: bool):
         """Decode path input: bf16 or fp64 on device (no cast kernel, no host
@@ -457,6 +448,34 @@ class DevicePredictor:
         a = self._fp64_args(xs, code, logits64=out64)
         check(lib().moep_predict_fp64(a, _stream(self.device)), "moep_predict_fp64")
         return out64
+
+
+# --------------------------------------------------------------- K0 input norm
+NORM_KINDS = {"none": 0, "rmsnorm": 1, "layernorm": 2}
+
+
+def input_norm(x: torch.Tensor, kind: str, gamma=None, beta=None, eps=None, status=None, device=None,
+               _force_exact=False) -> torch.Tensor:
+    """K0 (moep_input_norm): x [N, d] (bf16 / fp32 / fp64, on device) -> bf16 x_hat."""
+    if kind not in NORM_KINDS:
+        raise ConfigurationError(f"unknown norm kind {kind!r}")
+    dev = torch.device(device) if device is not None else x.device
+    eps = (1e-6 if kind == "rmsnorm" else 1e-5) if eps is None else eps
+    x = x.to(dev).contiguous()
+    if x.dim() != 2:
+        raise ConfigurationError(f"input shape {tuple(x.shape)} is not [N, d]")
+    code = {torch.bfloat16: MOEP_BF16, torch.float64: MOEP_F64, torch.float32: _lib.MOEP_F32}[x.dtype]
+    out = torch.empty(x.shape, dtype=torch.bfloat16, device=dev)
+    own = status is None
+    st = torch.zeros(2, dtype=torch.int32, device=dev) if own else status
+    g = None if gamma is None else torch.as_tensor(gamma, dtype=torch.float64).to(dev).contiguous()
+    b = None if beta is None else torch.as_tensor(beta, dtype=torch.float64).to(dev).contiguous()
+    k = NORM_KINDS[kind] | (0x100 if _force_exact else 0)
+    check(lib().moep_input_norm(ptr(x), code, x.shape[0], x.shape[1], k, ptr(g), ptr(b), float(eps), ptr(out),
+                                ptr(st), _stream(dev)), "moep_input_norm")
+    if own and int(st[0].item()):
+        raise ConfigurationError("input must be finite")
+    return out
 
 
 # ----------------------------------------------------------- logits kernels
