@@ -260,6 +260,8 @@ def main():
     synth = None
     if rank == 0 and not args.no_synthgen:
         synth = synthgen_arm(dev)
+    deploy = deploy_arm(layers[0], dev) if rank == 0 else None
+    c3 = c3_arm(dev) if rank == 0 and not args.no_prefetch else None
 
     if rank == 0:
         line = {
@@ -301,6 +303,8 @@ def main():
             "prefetch": prefetch,
             "train": train,
             "synthgen": synth,
+            "deploy": deploy,
+            "c3": c3,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -415,6 +419,133 @@ def cpu_baseline(model, x, truth, n_sample=32768):
     return {"value": n_sample / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"{n_sample} tokens of layer 0: predict_logits + top_k_batch(6) + evaluate_predictions "
                       f"(oracle/oracle.py numpy fp64, OpenBLAS all threads), {dt:.2f} s"}
+
+
+def deploy_arm(layer, dev, reps=5):
+    """The deployment predictor at the hook point (north_star (1)):
+    the decoder's hidden state through the input RMSNorm (K0, gamma, eps 1e-6,
+    x_hat bit-identical to oracle.input_norm_bf16) then the predictor pipeline
+    on x_hat (K1 + fix-up + counters), one 1M-token DSV2L layer; CUDA events."""
+    import torch
+    from oracle import oracle as O
+    from paper_2511_10676_b200.engine import input_norm
+    _, dp, x, truth = layer
+    h = (x.float() * 3.0 + 0.5).to(torch.bfloat16)           # pre-norm hidden state
+    gamma = np.random.default_rng(3).uniform(0.5, 1.5, D)
+    st = torch.zeros(2, dtype=torch.int32, device=dev)
+    kst = dp.new_status()
+    for _ in range(2):
+        xh = input_norm(h, "rmsnorm", gamma, status=st)
+        dp.evaluate(xh, truth, K_ACT, M_LIST, ids_m=K_ACT, status=kst)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    k0, pipe = [], []
+    for _ in range(reps):
+        ev[0].record()
+        xh = input_norm(h, "rmsnorm", gamma, status=st)
+        ev[1].record()
+        dp.evaluate(xh, truth, K_ACT, M_LIST, ids_m=K_ACT, status=kst)
+        ev[2].record()
+        torch.cuda.synchronize()
+        k0.append(ev[0].elapsed_time(ev[1]))
+        pipe.append(ev[1].elapsed_time(ev[2]))
+    dp.check_status(kst, xh)
+    rows = np.arange(0, h.shape[0], h.shape[0] // 256)
+    same = bool(np.array_equal(xh[rows].double().cpu().numpy(),
+                               O.input_norm_bf16(h[rows].double().cpu().numpy(), "rmsnorm", gamma)))
+    k0_ms, pipe_ms = statistics.median(k0), statistics.median(pipe)
+    n = h.shape[0]
+    return {"workload": "hook point: RMSNorm(gamma) -> x_hat (K0) -> predictor + top-6 + eval (one DSV2L layer)",
+            "tokens": n, "k0_ms": k0_ms, "k0_gbs": 4 * n * D / k0_ms / 1e6, "pipeline_ms": pipe_ms,
+            "tokens_per_s": n / ((k0_ms + pipe_ms) / 1e3), "x_hat_identical_to_oracle_rows": int(len(rows)) if same
+            else 0, "x_hat_identical": same}
+
+
+def c3_arm(dev, batches=(1, 8, 32, 128, 256), n_layers=48):
+    """BASELINE configs[2]: Qwen3-30B-A3B shape (d=2048, E=128, top-8), 48
+    MoE layers, decode batches. Per layer through deploy.HookPointPredictor:
+    K0 RMSNorm -> predictor top-8 (exact decode kernel for B <= 64, K1 +
+    fix-up above) on the main stream, then the layer's attention (decode GQA
+    stand-in: 32 query / 4 KV heads, head_dim 128, 4096 cached tokens) while
+    the predicted experts (9,437,184 B each) load on the copy engines into a
+    device cache (reset per layer: every layer has its own experts).
+    stall = max(0, load_end - attention_end) as pipesim.py:281-285. Ids of
+    every layer are checked against the exact fp64 path (and layer 0 against
+    the CPU oracle)."""
+    import torch
+    import paper_2511_10676_b200 as pb
+    import workloads as W
+    from oracle import oracle as O
+    from paper_2511_10676_b200 import prefetch as pf
+    from paper_2511_10676_b200.deploy import HookPointPredictor
+    from paper_2511_10676_b200.engine import topk_logits_device
+    E3, K3 = 128, 8
+    H_ = W.hadamard(D)
+    preds, models = [], []
+    for li in range(n_layers):
+        gate = W.gate_weights(E3, D, 30_000 + li)
+        m = pb.PredictorModel("arch2", H_ * 2.0 ** -W.GATE_SHIFT, np.zeros(D),
+                              W.round_bf16(gate @ H_.T * (2.0 ** (W.GATE_SHIFT + 1) / D)), np.zeros(E3),
+                              dropout_rate=0.0)
+        models.append(m)
+        preds.append(pb.DevicePredictor(m, dev))
+    gamma = np.random.default_rng(4).uniform(0.5, 1.5, D)
+    store = pf.ExpertStore(E3, pf.QWEN3_EXPERT_BYTES)
+    cache = pf.ExpertCache(E3, pf.QWEN3_EXPERT_BYTES, E3, device=dev)
+    prefetcher = pf.Prefetcher(store, cache)
+    hps = [HookPointPredictor(p_, K3, "rmsnorm", gamma, prefetcher=prefetcher) for p_ in preds]
+    main = torch.cuda.current_stream(dev)
+
+    def attention(qg, k, v):
+        s_ = torch.matmul(qg, k.transpose(-1, -2)) * (128 ** -0.5)
+        return torch.matmul(torch.softmax(s_.float(), dim=-1).to(qg.dtype), v)
+
+    out = {"config": "Qwen3-30B-A3B shape (d=2048, E=128, top-8), 48 layers, decode; oracle-gate predictors",
+           "expert_bytes": pf.QWEN3_EXPERT_BYTES, "batches": []}
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    for B in batches:
+        hid = (torch.randn((B, D), device=dev, generator=g) * 2.0 + 0.3).to(torch.bfloat16)
+        qb = torch.randn(B, 4, 8, 128, device=dev, dtype=torch.bfloat16)
+        kb = torch.randn(B, 4, 4096, 128, device=dev, dtype=torch.bfloat16)
+        vb = torch.randn(B, 4, 4096, 128, device=dev, dtype=torch.bfloat16)
+        for _ in range(2):
+            attention(qb, kb, vb)
+            hps[0].pre_attention(hid, prefetch=False)
+        torch.cuda.synchronize()
+        rows, mism = [], 0
+        for li in range(n_layers):
+            cache.reset()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record(main)
+            x_hat, ids = hps[li].pre_attention(hid, prefetch=False)
+            ev[1].record(main)
+            attention(qb, kb, vb)
+            ev[2].record(main)
+            hps[li].start_prefetch()          # the host reads the plan while the attention runs
+            ev[3].record(prefetcher.copy)
+            torch.cuda.synchronize()
+            t_pred = ev[0].elapsed_time(ev[1])
+            t_attn_end, t_load_end = ev[0].elapsed_time(ev[2]), ev[0].elapsed_time(ev[3])
+            n = int(prefetcher.need_count.item())
+            rows.append((t_pred, t_attn_end - t_pred, t_load_end - t_pred, max(0.0, t_load_end - t_attn_end), n))
+            z64 = preds[li].logits(x_hat)
+            mism += int((topk_logits_device(z64, K3) != ids).any(dim=1).sum())
+            hps[li].check()
+        # layer 0 against the CPU oracle: norm, then the predictor's top-8
+        m0 = models[0]
+        xo = O.input_norm_bf16(hid.double().cpu().numpy(), "rmsnorm", gamma)
+        ido = O.top_k_batch(O.predict_logits({"arch": "arch2", "w1": m0.w1, "b1": m0.b1, "w2": m0.w2, "b2": m0.b2},
+                                             xo), K3)
+        x0, i0 = hps[0].pre_attention(hid, prefetch=False)
+        oracle_ok = bool(np.array_equal(x0.double().cpu().numpy(), xo) and np.array_equal(i0.cpu().numpy(), ido))
+        r = np.array(rows)
+        out["batches"].append({"batch": B, "predict_ms": float(r[:, 0].mean()), "attention_ms": float(r[:, 1].mean()),
+                               "load_ms": float(r[:, 2].mean()), "stall_ms": float(r[:, 3].mean()),
+                               "experts_loaded": float(r[:, 4].mean()),
+                               "load_gbs": float(r[:, 4].mean() * pf.QWEN3_EXPERT_BYTES / (r[:, 2].mean() / 1e3) / 1e9),
+                               "ids_checked": B * n_layers, "ids_mismatch_vs_fp64": mism,
+                               "layer0_x_hat_and_ids_equal_oracle": oracle_ok})
+    return out
 
 
 def synthgen_arm(dev, n=262144, cpu_n=1024):

@@ -304,8 +304,14 @@ int moep_trace_ingest(const uint32_t* records, int64_t n, int32_t d, int32_t n_e
  * cache is full). Replaces the per-token load set of pipesim.schedule's
  * prefetch modes (pipesim.py:272-305), which the reference only models. */
 int moep_prefetch_plan(const int32_t* ids, int64_t n_ids, int32_t n_experts, const int32_t* slot_of,
-                       const int32_t* free_slots, int32_t n_free, uint8_t* mask_out, int32_t* need_list,
-                       int32_t* need_slot, int32_t* need_count, void* stream);
+                       const int32_t* free_slots, int32_t n_free, const int32_t* free_cursor, uint8_t* mask_out,
+                       int32_t* need_list, int32_t* need_slot, int32_t* need_count, void* stream);
+/* Residency update after a plan (device-only): slot_of[need_list[i]] =
+ * need_slot[i] for every assigned entry, *free_cursor += their number (the
+ * plan takes free slots from free_slots[*free_cursor ..]; NULL cursor = 0).
+ * plan -> K9 gather -> commit then runs with no host round trip. */
+int moep_prefetch_commit(const int32_t* need_list, const int32_t* need_slot, const int32_t* need_count,
+                         int32_t* slot_of, int32_t* free_cursor, void* stream);
 /* K9: GPU-driven copy of the listed experts from mapped pinned host memory
  * (expert e at host_mapped_store + e*expert_bytes) into cache slots. */
 int moep_gather_experts(const void* host_mapped_store, int64_t expert_bytes, const int32_t* need_list,

@@ -93,7 +93,8 @@ _SIGS = {
                         vp, vp, i32, vp],
     "moep_rows_dot": [vp, vp, vp, i64, i32, i32, vp, vp],
     "moep_bn_backward": [vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp],
-    "moep_prefetch_plan": [vp, i64, i32, vp, vp, i32, vp, vp, vp, vp, vp],
+    "moep_prefetch_plan": [vp, i64, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp],
+    "moep_prefetch_commit": [vp, vp, vp, vp, vp, vp],
     "moep_gather_experts": [vp, i64, vp, vp, vp, vp, i32, vp],
     "moep_trace_ingest": [vp, i64, i32, i32, i32, i32, vp, vp, vp, i64, vp, vp],
     "moep_teacher_normals": [C.c_uint64, i64, i64, i32, i32, vp, vp, vp, vp],

@@ -22,8 +22,13 @@ namespace pf {
 
 __global__ void __launch_bounds__(1024)
 plan_kernel(const int32_t* __restrict__ ids, int64_t n_ids, int32_t E, const int32_t* __restrict__ slot_of,
-            const int32_t* __restrict__ free_slots, int32_t n_free, uint8_t* __restrict__ mask_out,
-            int32_t* __restrict__ need_list, int32_t* __restrict__ need_slot, int32_t* __restrict__ need_count) {
+            const int32_t* __restrict__ free_slots, int32_t n_free, const int32_t* __restrict__ free_cursor,
+            uint8_t* __restrict__ mask_out, int32_t* __restrict__ need_list, int32_t* __restrict__ need_slot,
+            int32_t* __restrict__ need_count) {
+  // free slots start at the device cursor (moep_prefetch_commit advances it)
+  const int32_t cur = free_cursor ? *free_cursor : 0;
+  free_slots += cur;
+  n_free -= cur;
   extern __shared__ uint8_t bm[];  // [E] union bitmap (bytes)
   __shared__ int warp_base[32];
   for (int e = threadIdx.x; e < E; e += blockDim.x) bm[e] = 0;
@@ -61,6 +66,22 @@ plan_kernel(const int32_t* __restrict__ ids, int64_t n_ids, int32_t E, const int
   if (threadIdx.x == 0) *need_count = total;
 }
 
+// Residency update after a plan (one warp): slot_of[need_list[i]] = need_slot[i]
+// for the assigned entries, free-slot cursor += their number. Device-only, so
+// plan -> load -> commit needs no host round trip.
+__global__ void commit_kernel(const int32_t* __restrict__ need_list, const int32_t* __restrict__ need_slot,
+                              const int32_t* __restrict__ need_count, int32_t* __restrict__ slot_of,
+                              int32_t* __restrict__ free_cursor) {
+  const int count = *need_count;
+  int assigned = 0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    const int s = need_slot[i];
+    if (s >= 0) { slot_of[need_list[i]] = s; ++assigned; }
+  }
+  for (int o = 16; o > 0; o >>= 1) assigned += __shfl_xor_sync(0xffffffffu, assigned, o);
+  if (threadIdx.x == 0) *free_cursor += assigned;
+}
+
 // One CTA per (expert, chunk): 16-byte loads from mapped host memory.
 __global__ void __launch_bounds__(512)
 gather_kernel(const uint4* __restrict__ host_store, int64_t expert_bytes, const int32_t* __restrict__ need_list,
@@ -94,13 +115,21 @@ gather_kernel(const uint4* __restrict__ host_store, int64_t expert_bytes, const 
 extern "C" {
 
 int moep_prefetch_plan(const int32_t* ids, int64_t n_ids, int32_t n_experts, const int32_t* slot_of,
-                       const int32_t* free_slots, int32_t n_free, uint8_t* mask_out, int32_t* need_list,
-                       int32_t* need_slot, int32_t* need_count, void* stream) {
+                       const int32_t* free_slots, int32_t n_free, const int32_t* free_cursor, uint8_t* mask_out,
+                       int32_t* need_list, int32_t* need_slot, int32_t* need_count, void* stream) {
   if (n_ids < 0 || n_experts <= 0 || n_experts > 65536) return MOEP_ESHAPE;
   if (!ids || !need_list || !need_count) return MOEP_EARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  moep::pf::plan_kernel<<<1, 992, n_experts, st>>>(ids, n_ids, n_experts, slot_of, free_slots, n_free, mask_out,
-                                                  need_list, need_slot, need_count);
+  moep::pf::plan_kernel<<<1, 992, n_experts, st>>>(ids, n_ids, n_experts, slot_of, free_slots, n_free, free_cursor,
+                                                  mask_out, need_list, need_slot, need_count);
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+int moep_prefetch_commit(const int32_t* need_list, const int32_t* need_slot, const int32_t* need_count,
+                         int32_t* slot_of, int32_t* free_cursor, void* stream) {
+  if (!need_list || !need_slot || !need_count || !slot_of || !free_cursor) return MOEP_EARG;
+  moep::pf::commit_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(need_list, need_slot, need_count,
+                                                                          slot_of, free_cursor);
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }
 

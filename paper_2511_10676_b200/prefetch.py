@@ -75,10 +75,11 @@ class ExpertCache:
         self.data = torch.empty(n_slots * expert_bytes, dtype=torch.uint8, device=self.dev)
         self.slot_of = torch.full((n_experts,), -1, dtype=torch.int32, device=self.dev)
         self.free_slots = torch.arange(n_slots, dtype=torch.int32, device=self.dev)
+        self.free_cursor = torch.zeros(1, dtype=torch.int32, device=self.dev)  # next free slot (device)
 
     def reset(self):
         self.slot_of.fill_(-1)
-        self.free_slots = torch.arange(self.n_slots, dtype=torch.int32, device=self.dev)
+        self.free_cursor.zero_()
 
     def slot(self, s: int) -> torch.Tensor:
         return self.data[s * self.expert_bytes:(s + 1) * self.expert_bytes]
@@ -103,20 +104,17 @@ class Prefetcher:
         ids = ids.to(device=self.dev, dtype=torch.int32).contiguous()
         c = self.cache
         check(lib().moep_prefetch_plan(ptr(ids), ids.numel(), self.store.n_experts, ptr(c.slot_of),
-                                       ptr(c.free_slots), c.free_slots.numel(), ptr(self.mask),
+                                       ptr(c.free_slots), c.free_slots.numel(), ptr(c.free_cursor), ptr(self.mask),
                                        ptr(self.need_list), ptr(self.need_slot), ptr(self.need_count),
                                        _stream(st)), "moep_prefetch_plan")
 
-    def _commit_residency(self, n_loaded: int | None = None):
-        """Mark loaded experts resident (device-side table update, no sync)."""
+    def commit(self, stream=None):
+        """Mark the planned experts resident: a device-side table update on
+        `stream` (default: the copy stream), no host synchronisation."""
+        st = stream or self.copy
         c = self.cache
-        n = int(self.need_count.item()) if n_loaded is None else n_loaded
-        if n:
-            e = self.need_list[:n].long()
-            s = self.need_slot[:n]
-            ok = s >= 0
-            c.slot_of[e[ok]] = s[ok]
-            c.free_slots = c.free_slots[int(ok.sum().item()):]
+        check(lib().moep_prefetch_commit(ptr(self.need_list), ptr(self.need_slot), ptr(self.need_count),
+                                         ptr(c.slot_of), ptr(c.free_cursor), _stream(st)), "moep_prefetch_commit")
 
     def load_copy_engine(self, ids: torch.Tensor) -> int:
         """Plan on the copy stream, read the plan on the host, one cudaMemcpyAsync
@@ -137,17 +135,20 @@ class Prefetcher:
             for e, s in zip(lst, slots):
                 if s >= 0:
                     self.cache.slot(s).copy_(self.store.blob(e), non_blocking=True)
+            self.commit(self.copy)
             self.done.record(self.copy)
         return n
 
     def load_sm_gather(self, ids: torch.Tensor, n_ctas: int = 64) -> None:
-        """K8 + K9 on the copy stream; no host round trip. Completion: self.done."""
+        """K8 + K9 + residency commit on the copy stream; no host round trip.
+        Completion: self.done."""
         with torch.cuda.stream(self.copy):
             self.plan(ids, self.copy)
             check(lib().moep_gather_experts(self.store.host.data_ptr(), self.store.expert_bytes,
                                             ptr(self.need_list), ptr(self.need_slot), ptr(self.need_count),
                                             ptr(self.cache.data), n_ctas, _stream(self.copy)),
                   "moep_gather_experts")
+            self.commit(self.copy)
             self.done.record(self.copy)
 
 

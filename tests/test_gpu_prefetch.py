@@ -55,7 +55,55 @@ def test_loads_land_in_slots(pf, path):
     assert lst == [3, 9, 11, 12, 15]
     for e, s in zip(lst, slots):
         assert torch.equal(cache.slot(s).cpu(), store.blob(e)), (e, s)
-    p._commit_residency()
+    # residency was committed on the device by the load path itself
+    assert cache.slot_of[torch.tensor(lst).cuda().long()].cpu().tolist() == slots
+    assert int(cache.free_cursor.item()) == 5
     p.plan(torch.tensor([[3, 4]], dtype=torch.int32).cuda())
     torch.cuda.synchronize()
     assert p.need_list[: int(p.need_count.item())].cpu().tolist() == [4]
+    assert p.need_slot[:1].cpu().tolist() == [5]   # the next free slot (device cursor)
+
+
+def test_hook_point_deployment(pf):
+    """SURVEY 8(f)1 (hooks.py:19,113-114; pipesim.py:272-305 executed): raw
+    hidden states -> K0 RMSNorm(gamma) -> x_hat bit-identical to the oracle ->
+    predicted top-m identical to the oracle's on x_hat -> those experts in the
+    cache with the right bytes; after the router, exactly the missed experts
+    are loaded and every true expert has a slot holding its blob."""
+    import paper_2511_10676_b200 as pb
+    from paper_2511_10676_b200.deploy import HookPointPredictor
+    from oracle import oracle as O
+    rng = np.random.default_rng(5)
+    d, h, E, m, k, B = 512, 512, 32, 4, 3, 5
+    model = pb.init_model("arch2", d, h, E, seed=2)
+    model.w1, model.w2 = O.round_bf16(model.w1), O.round_bf16(model.w2)
+    gamma = rng.uniform(0.5, 1.5, d)
+    for gather in (0, 16):
+        store = pf.ExpertStore(E, 8192)
+        cache = pf.ExpertCache(E, 8192, E)
+        hp = HookPointPredictor(model, m, "rmsnorm", gamma, prefetcher=pf.Prefetcher(store, cache), gather_ctas=gather)
+        hidden = O.round_bf16(2.0 * rng.standard_normal((B, d)) + 0.3)
+        x_hat, ids = hp.pre_attention(torch.from_numpy(hidden).cuda().to(torch.bfloat16))
+        xo = O.input_norm_bf16(hidden, "rmsnorm", gamma)
+        assert np.array_equal(x_hat.double().cpu().numpy(), xo)
+        p = {"arch": "arch2", "w1": model.w1, "b1": model.b1, "w2": model.w2, "b2": model.b2}
+        want = O.top_k_batch(O.predict_logits(p, xo), m)
+        assert np.array_equal(ids.cpu().numpy(), want)
+        hp.pf.done.synchronize()
+        predicted = sorted(set(want.ravel().tolist()))
+        slot_of = cache.slot_of.cpu().numpy()
+        for e in predicted:
+            assert slot_of[e] >= 0 and torch.equal(cache.slot(int(slot_of[e])).cpu(), store.blob(e)), e
+        true = np.sort(np.stack([rng.choice(E, k, replace=False) for _ in range(B)]), axis=1)
+        slots, n_emergency = hp.post_router(torch.from_numpy(true).cuda().to(torch.int32))
+        torch.cuda.synchronize()
+        assert n_emergency == len(set(true.ravel().tolist()) - set(predicted))
+        for e, s in zip(true.ravel().tolist(), slots.cpu().numpy().ravel().tolist()):
+            assert s >= 0 and torch.equal(cache.slot(int(s)).cpu(), store.blob(e)), e
+        hp.check()
+    bad = torch.zeros((2, d), dtype=torch.bfloat16, device="cuda")
+    bad[1, 3] = float("inf")
+    hp2 = HookPointPredictor(model, m, "rmsnorm", gamma)
+    hp2.pre_attention(bad)
+    with pytest.raises(pb.ConfigurationError):
+        hp2.check()
