@@ -29,13 +29,26 @@ def allreduce_counters(counters: torch.Tensor, group=None) -> torch.Tensor:
     return counters
 
 
-def dp_hooks(group=None):
-    """(grad_allreduce, loss_allreduce) callables for trainer.train / DeviceTrainer."""
+def dp_hooks(group=None, host_staged: bool = False):
+    """(grad_allreduce, loss_allreduce) callables for trainer.train / DeviceTrainer.
 
-    def grad_allreduce(flat_grad: torch.Tensor):
-        dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM, group=group)
+    host_staged: copy through host memory around the collective (a gloo
+    process group; the CPU tests and the one-GPU multi-process test)."""
 
-    def loss_allreduce(partial_sums: torch.Tensor):
-        dist.all_reduce(partial_sums, op=dist.ReduceOp.SUM, group=group)
+    def _ar(t: torch.Tensor):
+        if host_staged and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
-    return grad_allreduce, loss_allreduce
+    return _ar, _ar
+
+
+def allreduce_counters_host(counters: torch.Tensor, group=None) -> torch.Tensor:
+    """allreduce_counters through host memory (gloo)."""
+    h = counters.cpu()
+    allreduce_counters(h, group)
+    counters.copy_(h)
+    return counters
