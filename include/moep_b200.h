@@ -329,6 +329,11 @@ int moep_teacher_normals(uint64_t seed, int64_t first_index, int64_t n, int32_t 
 /* core.layer_norm (core.py:57-68) row-wise over [n, d] fp64 with numpy's
  * reduction order (0 + pairwise_sum) and single roundings: bit-identical to
  * numpy. out may alias x. */
+/* fp64 GEMM on the fp64 tensor cores: C[M, N] = epi(A[M, K] . B[N, K]^T),
+ * row-major with leading dimensions, epi 0 = identity, 1 = tanh. The
+ * teacher's dense maps (synthgen.py:176-189: mix, tanh(W_in x), W_out, gate). */
+int moep_dgemm_nt(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                  int64_t M, int64_t N, int64_t K, int32_t epilogue, void* stream);
 int moep_layer_norm_np(const double* x, int64_t n, int32_t d, double eps, double* out, void* stream);
 /* core.softmax (core.py:19-24) over the rows of an fp64 [n, E] array in
  * numpy's order (max, exp, 0 + pairwise_sum, divide); out may alias z. */

@@ -99,6 +99,7 @@ _SIGS = {
     "moep_trace_ingest": [vp, i64, i32, i32, i32, i32, vp, vp, vp, i64, vp, vp],
     "moep_teacher_normals": [C.c_uint64, i64, i64, i32, i32, vp, vp, vp, vp],
     "moep_layer_norm_np": [vp, i64, i32, f64, vp, vp],
+    "moep_dgemm_nt": [vp, i64, vp, i64, vp, i64, i64, i64, i64, i32, vp],
     "moep_softmax_np": [vp, i64, i32, vp, vp],
     "moep_teacher_finish": [vp, i64, i32, i32, vp, vp, vp],
     "moep_num_sms": [],

@@ -117,14 +117,22 @@ class _Teacher:
     def __init__(self, spec: TeacherSpec, device):
         self.spec = spec
         self.dev = torch.device(device)
-        self.gate_t = torch.as_tensor(spec.router.gate_weights).to(self.dev).t()   # [d, E]
-        self.mix_t = self.w_in_t = self.w_out_t = None
+        # row-major [N, K] operands of moep_dgemm_nt (C = A . B^T)
+        f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(self.dev)
+        self.gate = f64(spec.router.gate_weights)            # [E, d]
+        self.mix = self.w_in = self.w_out = None
         if spec.transform == "linear":
-            self.mix_t = torch.as_tensor(spec.mix_matrix).to(self.dev).t()
+            self.mix = f64(spec.mix_matrix)                   # [d, d]: x @ M^T
         elif spec.transform == "nonlinear":
             w_in, w_out = _nonlinear_maps(spec)
-            self.w_in_t = torch.as_tensor(w_in).to(self.dev).t()
-            self.w_out_t = torch.as_tensor(w_out).to(self.dev).t()
+            self.w_in, self.w_out = f64(w_in), f64(w_out)     # [h, d], [d, h]
+
+    def _gemm(self, a: torch.Tensor, b: torch.Tensor, tanh: bool = False) -> torch.Tensor:
+        """a [M, K] . b[N, K]^T on the fp64 tensor cores (moep_dgemm_nt)."""
+        c = torch.empty((a.shape[0], b.shape[0]), dtype=torch.float64, device=self.dev)
+        check(lib().moep_dgemm_nt(ptr(a), a.stride(0), ptr(b), b.stride(0), ptr(c), c.stride(0), a.shape[0],
+                                  b.shape[0], a.shape[1], int(tanh), _stream(self.dev)), "moep_dgemm_nt")
+        return c
 
     def chunk(self, first: int, n: int, acts32: torch.Tensor, scores: torch.Tensor, topk: torch.Tensor):
         """Samples first .. first+n-1 into the given output row views."""
@@ -138,15 +146,15 @@ class _Teacher:
         if sp.transform == "identity":
             post = x64                                  # x.copy(): x64 is not needed afterwards
         elif sp.transform == "linear":
-            post = torch.mm(x64, self.mix_t)
+            post = self._gemm(x64, self.mix)
         else:
-            post = torch.mm(torch.tanh(torch.mm(x64, self.w_in_t)), self.w_out_t)
+            post = self._gemm(self._gemm(x64, self.w_in, tanh=True), self.w_out)
         if noisy:
             post.add_(nz.mul_(sp.noise_sigma))          # post += sigma * noise: two roundings, as numpy
         if sp.post_norm:
             check(lib().moep_layer_norm_np(ptr(post), n, d, LAYER_NORM_EPS, ptr(post), _stream(dev)),
                   "moep_layer_norm_np")
-        logits = torch.mm(post, self.gate_t)
+        logits = self._gemm(post, self.gate)
         check(lib().moep_teacher_finish(ptr(logits), n, E, k, ptr(scores), ptr(topk), _stream(dev)),
               "moep_teacher_finish")
 

@@ -130,3 +130,23 @@ def test_softmax_numpy_order():
         np.testing.assert_allclose(got, want, rtol=4e-16 * 8, atol=0)
     z = rng.standard_normal((1000, 64))
     assert np.array_equal(np.argsort(-pb.softmax(z), axis=1, kind="stable"), np.argsort(-z, axis=1, kind="stable"))
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(1000, 64, 2048, 0), (333, 130, 77, 1), (4096, 2048, 512, 0), (7, 5, 3, 1)])
+def test_dgemm_nt_vs_numpy(M, N, K, epi):
+    """moep_dgemm_nt (the teacher's GEMMs on the fp64 tensor cores) against
+    numpy float64, ragged shapes and the tanh epilogue."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2511_10676_b200._lib import check, lib, ptr
+    rng = np.random.default_rng(M + N + K)
+    a = rng.standard_normal((M, K))
+    b = rng.standard_normal((N, K)) / np.sqrt(K)
+    at, bt = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    check(lib().moep_dgemm_nt(ptr(at), K, ptr(bt), K, ptr(c), N, M, N, K, epi,
+                              torch.cuda.current_stream().cuda_stream), "moep_dgemm_nt")
+    ref = a @ b.T
+    if epi:
+        ref = np.tanh(ref)
+    assert np.allclose(c.cpu().numpy(), ref, rtol=1e-12, atol=1e-13)

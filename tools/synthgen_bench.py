@@ -97,7 +97,7 @@ def main():
         ev[1].record()
         check(lib().moep_layer_norm_np(ptr(x64c), c, d, 1e-5, ptr(x64c), st), "ln")
         ev[2].record()
-        logits = torch.mm(x64c, tt.gate_t)
+        logits = tt._gemm(x64c, tt.gate)  # moep_dgemm_nt (fp64 tensor cores)
         ev[3].record()
         check(lib().moep_teacher_finish(ptr(logits), c, e, k, ptr(sc), ptr(tk), st), "finish")
         ev[4].record()
