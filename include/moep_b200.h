@@ -334,6 +334,19 @@ int moep_teacher_normals(uint64_t seed, int64_t first_index, int64_t n, int32_t 
  * teacher's dense maps (synthgen.py:176-189: mix, tanh(W_in x), W_out, gate). */
 int moep_dgemm_nt(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                   int64_t M, int64_t N, int64_t K, int32_t epilogue, void* stream);
+/* C[M, N] = A[K, M]^T . B[K, N] in fp64 on the fp64 tensor cores (the fp64
+ * training mode's dW1 = dA^T X, predictor.py:295). */
+int moep_dgemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                  int64_t M, int64_t N, int64_t K, void* stream);
+/* dW1 of the tensor-core training modes (predictor.py:295) on tcgen05:
+ * dw1[h, d] = sum_n dA[n, p*h + j] X[n, i] summed over the p < passes column
+ * blocks of dA (passes 2: the fp32 mode's bf16 hi | lo halves), fp32 out.
+ * dA [n, passes*h] and X [n, d] bf16 row-major (token-major). workspace:
+ * moep_dw1_workspace_floats(...) floats for the K-split partials (0: none
+ * needed; too small a workspace disables the split). */
+int64_t moep_dw1_workspace_floats(int32_t hidden, int32_t d, int64_t n_tokens, int32_t passes);
+int moep_dw1_bf16(const void* da, const void* x, int64_t n_tokens, int32_t hidden, int32_t d, int32_t passes,
+                  float* dw1, float* workspace, int64_t workspace_floats, void* stream);
 int moep_layer_norm_np(const double* x, int64_t n, int32_t d, double eps, double* out, void* stream);
 /* core.softmax (core.py:19-24) over the rows of an fp64 [n, E] array in
  * numpy's order (max, exp, 0 + pairwise_sum, divide); out may alias z. */

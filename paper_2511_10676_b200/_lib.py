@@ -100,12 +100,15 @@ _SIGS = {
     "moep_teacher_normals": [C.c_uint64, i64, i64, i32, i32, vp, vp, vp, vp],
     "moep_layer_norm_np": [vp, i64, i32, f64, vp, vp],
     "moep_dgemm_nt": [vp, i64, vp, i64, vp, i64, i64, i64, i64, i32, vp],
+    "moep_dgemm_tn": [vp, i64, vp, i64, vp, i64, i64, i64, i64, vp],
+    "moep_dw1_workspace_floats": [i32, i32, i64, i32],
+    "moep_dw1_bf16": [vp, vp, i64, i32, i32, i32, vp, vp, i64, vp],
     "moep_softmax_np": [vp, i64, i32, vp, vp],
     "moep_teacher_finish": [vp, i64, i32, i32, vp, vp, vp],
     "moep_num_sms": [],
     "moep_version": [],
 }
-_RESTYPES = {"moep_version": C.c_char_p, "moep_predict_split_floats": i64}
+_RESTYPES = {"moep_version": C.c_char_p, "moep_predict_split_floats": i64, "moep_dw1_workspace_floats": i64}
 EXPORTED = tuple(_SIGS)
 
 _lib = None

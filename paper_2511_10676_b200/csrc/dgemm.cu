@@ -27,8 +27,9 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 
 // TM x TN tile (64 x 128, or 128 x 64 when N <= 64: the gate's E columns),
-// warps WM x WN = (TM / 32) x (TN / 32)
-template <int EPI, int TM, int TN>
+// warps WM x WN = (TM / 32) x (TN / 32). TN_MODE: A is [K, M] and B [K, N]
+// (C = A^T . B: the fp64 training mode's dW1 = dA^T X, predictor.py:295).
+template <int EPI, int TM, int TN, bool TN_MODE = false>
 __global__ void __launch_bounds__(NT, 2)
 dgemm_nt_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B, int64_t ldb,
                 double* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K) {
@@ -45,8 +46,25 @@ dgemm_nt_kernel(const double* __restrict__ A, int64_t lda, const double* __restr
   const int br = tid & (TN - 1), bkh = tid / TN;
   const int64_t arow = m0 + ar, brow = n0 + br;
   const bool vec = ((lda | ldb) & 1) == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
-  double ra[AK], rb[BK];
+  double ra[AK > TM / 16 ? AK : TM / 16], rb[BK > TN / 16 ? BK : TN / 16];
+  // TN mode loaders: thread = (k row tid / 16, MN run of TM/16 or TN/16 from (tid % 16))
+  constexpr int AR = TM / 16, BR = TN / 16;
+  auto fetch_t = [&](int64_t k0) {
+    const int64_t kk = k0 + tid / 16;
+    const int64_t ma = m0 + (tid % 16) * AR, nb = n0 + (tid % 16) * BR;
+#pragma unroll
+    for (int c = 0; c < AR; ++c) ra[c] = (kk < K && ma + c < M) ? A[kk * lda + ma + c] : 0.0;
+#pragma unroll
+    for (int c = 0; c < BR; ++c) rb[c] = (kk < K && nb + c < N) ? B[kk * ldb + nb + c] : 0.0;
+  };
+  auto stash_t = [&](int buf) {
+#pragma unroll
+    for (int c = 0; c < AR; ++c) As[buf][(tid / 16) * AP + (tid % 16) * AR + c] = ra[c];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) Bs[buf][(tid / 16) * BP + (tid % 16) * BR + c] = rb[c];
+  };
   auto fetch = [&](int64_t k0) {
+    if (TN_MODE) { fetch_t(k0); return; }
     const int64_t ka = k0 + akq * AK, kb = k0 + bkh * BK;
     if (vec && arow < M && ka + AK <= K) {
       const double2* p = reinterpret_cast<const double2*>(A + arow * lda + ka);
@@ -66,6 +84,7 @@ dgemm_nt_kernel(const double* __restrict__ A, int64_t lda, const double* __restr
     }
   };
   auto stash = [&](int buf) {
+    if (TN_MODE) { stash_t(buf); return; }
 #pragma unroll
     for (int c = 0; c < AK; ++c) As[buf][(akq * AK + c) * AP + ar] = ra[c];
 #pragma unroll
@@ -150,5 +169,26 @@ extern "C" int moep_dgemm_nt(const double* A, int64_t lda, const double* B, int6
     attr[ki] = true;
   }
   kerns[ki]<<<grid, moep::dg::NT, sm, st>>>(A, lda, B, ldb, C, ldc, M, N, K);
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
+// C[M, N] = A[K, M]^T . B[K, N] (row-major operands, token-major: the fp64
+// training mode's dW1 = dA^T X, predictor.py:295)
+extern "C" int moep_dgemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                             int64_t M, int64_t N, int64_t K, void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || lda < M || ldb < N || ldc < N) return MOEP_ESHAPE;
+  if (!A || !B || !C) return MOEP_EARG;
+  const int64_t gy = (M + 63) / 64, gx = (N + 127) / 128;
+  if (gy > 65535) return MOEP_EUNSUPPORTED;
+  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
+  const size_t sm = 2 * moep::dg::KS * (64 + 4 + 128 + 4) * sizeof(double);
+  static bool attr = false;
+  auto kern = moep::dg::dgemm_nt_kernel<0, 64, 128, true>;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)) != cudaSuccess)
+      return MOEP_ELAUNCH;
+    attr = true;
+  }
+  kern<<<grid, moep::dg::NT, sm, static_cast<cudaStream_t>(stream)>>>(A, lda, B, ldb, C, ldc, M, N, K);
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }

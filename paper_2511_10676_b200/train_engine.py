@@ -14,7 +14,8 @@ Precision modes:
           (trainer.py:131-204, predictor.py:193-327).
   "fp32"  throughput mode (arch2): forward K1 (bf16 tcgen05 GEMMs with the hi/lo
           GEMM2, fp32 pre-activations), K4 on fp32 logits (fp64 math), K5 fp32,
-          dW1 = dA^T X on bf16 tensor cores with dA split hi+lo (fp32 out),
+          dW1 = dA^T X on the tcgen05 tensor cores (moep_dw1_bf16, MN-major
+          operands straight from K5's dA and the input) with dA split hi+lo,
           fp32 master weights and Adam moments.
 One step = forward, loss (+ optional all-reduce of the 3 loss partial sums for
 batch-global normalisers), backward, optional gradient all-reduce, optimizer.
@@ -80,6 +81,7 @@ class DeviceTrainer:
             self.dropout_seed = int(model.dropout_seed) & 0xFFFFFFFFFFFFFFFF
             self.dropout_step = int(getattr(model, "_dropout_step", 0))
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self._dw1_ws = None  # K-split partials of the tcgen05 dW1 GEMM
         self.t = 0
         self.grad_allreduce, self.loss_allreduce = grad_allreduce, loss_allreduce
         self.n_sms = lib().moep_num_sms()
@@ -190,26 +192,21 @@ class DeviceTrainer:
                       "moep_act_backward_bf16split")
         gw1 = self.view(self.grad, 0)
         if self.precision == "fp64":
+            # fp64 dW1 = dA^T X on the fp64 tensor cores (moep_dgemm_tn)
             xs = x_used if x_used.dtype == torch.float64 else x_used.to(torch.float64)
-            torch.mm(da.t(), xs, out=gw1)  # plain fp64 GEMM (cuBLAS DGEMM)
-        elif self.arch == "arch1":
-            hi = da.to(torch.bfloat16)
-            lo = (da - hi.float()).to(torch.bfloat16)
-            self._dw1_hilo(hi, lo, x_used, gw1)
-        elif self.precision == "bf16":
-            gw1.copy_(torch.mm(da.t(), x_used, out_dtype=torch.float32))
+            xs = xs.contiguous()
+            check(lib().moep_dgemm_tn(ptr(da), H, ptr(xs), self.d, ptr(gw1), self.d, H, self.d, n,
+                                      _stream(self.dev)), "moep_dgemm_tn")
         else:
-            # one bf16 GEMM over the [hi | lo] rows: C = [hi^T X ; lo^T X], fp32
-            c = torch.mm(da.t(), x_used, out_dtype=torch.float32)
-            torch.add(c[:H], c[H:], out=gw1)
+            # tcgen05 dW1 (moep_dw1_bf16): dA leaves K5 as bf16 [n, P*h] (P = 2: hi | lo)
+            passes = 2 if self.precision == "fp32" else 1
+            need = int(lib().moep_dw1_workspace_floats(H, self.d, n, passes))
+            if need and (self._dw1_ws is None or self._dw1_ws.numel() < need):
+                self._dw1_ws = torch.empty(need, dtype=torch.float32, device=self.dev)
+            ws = self._dw1_ws if need else None
+            check(lib().moep_dw1_bf16(ptr(da), ptr(x_used.contiguous()), n, H, self.d, passes, ptr(gw1), ptr(ws),
+                                      ws.numel() if ws is not None else 0, _stream(self.dev)), "moep_dw1_bf16")
         return da
-
-    @staticmethod
-    def _dw1_hilo(hi, lo, x, gw1):
-        """dW1 = hi^T X + lo^T X on bf16 tensor cores, fp32 accumulate (cuBLAS,
-        the second GEMM accumulating into the first's output)."""
-        acc = torch.mm(hi.t(), x, out_dtype=torch.float32)
-        gw1.copy_(torch.addmm(acc, lo.t(), x, out_dtype=torch.float32))
 
     # -------------------------------------------------------------- step
     def optimizer_step(self):
