@@ -428,6 +428,8 @@ def train_arch2(acts, scores, topk, k, *, hidden=32, batch_size=64, epochs=1, lr
             else:
                 z, cache = forward_eval(p, x_tr[b])  # arch2 train forward == eval forward
             lv, dz = loss_and_grad(loss, z, lb)
+            if not np.isfinite(lv):  # trainer.py:184-185
+                raise FloatingPointError(f"non-finite loss at step {steps}")
             g = backward_train_arch1(p, cache, dz) if arch == "arch1" else backward_eval(p, cache, dz)
             g = {kk: g[kk] for kk in names}
             t += 1
@@ -435,6 +437,9 @@ def train_arch2(acts, scores, topk, k, *, hidden=32, batch_size=64, epochs=1, lr
                 adam_step(p, g, state, t, lr=lr)
             else:
                 sgd_step(p, g, state, lr, momentum=0.9 if optimizer == "momentum" else None)
+            for nm in names:  # _nan_guard, trainer.py:125-128
+                if not np.all(np.isfinite(p[nm])):
+                    raise FloatingPointError(f"non-finite {nm} after step {steps}")
             loss_sum += lv * len(b)
             steps += 1
             if max_steps and steps >= max_steps:

@@ -664,6 +664,9 @@ static bool use_v4(const moep_predict_args* a) {
 static int choose_split(int64_t n_tokens, int nchunks, int n_pairs) {
   const int64_t tiles = (n_tokens + 2 * BM - 1) / (2 * BM);
   if (tiles >= n_pairs) return 1;
+#ifdef MOEP_FORCE_SPLIT2
+  if (nchunks % 2 == 0) return 2;
+#endif
   const int64_t cost1 = ((tiles + n_pairs - 1) / n_pairs) * nchunks;
   int best = 1;
   int64_t best_cost = cost1;

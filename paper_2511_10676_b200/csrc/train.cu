@@ -912,24 +912,37 @@ int moep_act_backward_bf16split(const float* a, const float* dz, const float* w2
     if (!with_lo) return MOEP_EUNSUPPORTED;
     return act_backward_t<float, true>(a, dz, w2, n, H, E, n_slices, nullptr, out, dw2, db1, db2, scratch, st);
   }
-  const int rows_per_slice = static_cast<int>((n + n_slices - 1) / n_slices);
-  float* dw2_part = scratch;
-  float* db1_part = dw2_part + static_cast<int64_t>(n_slices) * E * H;
-  float* db2_part = db1_part + static_cast<int64_t>(n_slices) * H;
-  dim3 grid((H / 2 + 127) / 128, n_slices);
+  const int gx = (H / 2 + 127) / 128;
   constexpr int kAbuf = 2 * BR * 256 * 4;  // staging for `a`
+  // row slices: one resident wave (the occupancy calculator's blocks per SM x
+  // SMs, divided over the column blocks), at most the caller's n_slices (its
+  // scratch size). 128 slices ran 1.4 waves at H = 2048 (87 us per 16 k Phi rows).
+  auto slices_for = [&](const void* kern) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, kAbuf) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    const int fit = per_sm * moep_num_sms() / gx;
+    return fit < 1 ? 1 : (fit < n_slices ? fit : n_slices);
+  };
 #define MOEP_K5X2(EM, LOV)                                                                                     \
   do {                                                                                                         \
     if (cudaFuncSetAttribute(act_backward_f32x2_kernel<EM, LOV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              kAbuf) != cudaSuccess)                                                            \
       return MOEP_ELAUNCH;                                                                                     \
-    act_backward_f32x2_kernel<EM, LOV><<<grid, 128, kAbuf, st>>>(a, dz, w2, n, H, E, rows_per_slice, out,      \
-                                                                  dw2_part, db1_part, db2_part);               \
+    ns = slices_for(reinterpret_cast<const void*>(act_backward_f32x2_kernel<EM, LOV>));                       \
+    rows_per_slice = static_cast<int>((n + ns - 1) / ns);                                                      \
+    dw2_part = scratch;                                                                                        \
+    db1_part = dw2_part + static_cast<int64_t>(ns) * E * H;                                                    \
+    db2_part = db1_part + static_cast<int64_t>(ns) * H;                                                        \
+    act_backward_f32x2_kernel<EM, LOV><<<dim3(gx, ns), 128, kAbuf, st>>>(a, dz, w2, n, H, E, rows_per_slice,  \
+                                                                        out, dw2_part, db1_part, db2_part);   \
   } while (0)
+  int ns = n_slices, rows_per_slice = 0;
+  float *dw2_part = nullptr, *db1_part = nullptr, *db2_part = nullptr;
   if (E <= 16) { if (with_lo) MOEP_K5X2(16, true); else MOEP_K5X2(16, false); }
   else { if (with_lo) MOEP_K5X2(32, true); else MOEP_K5X2(32, false); }
 #undef MOEP_K5X2
-  sum_parts3<float>(dw2_part, db1_part, db2_part, n_slices, E, H, dw2, db1, db2, st);
+  sum_parts3<float>(dw2_part, db1_part, db2_part, ns, E, H, dw2, db1, db2, st);
   return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
 }
 

@@ -130,6 +130,9 @@ class DeviceTrainer:
             A.w2 = ptr(self.shadow[self.H * self.d:])
             A.b1, A.b2 = ptr(self.view(self.flat, 2)), ptr(self.view(self.flat, 3))
             A.logits, A.flags, A.flag_list, A.flag_count, A.a_out = ptr(z), ptr(flags), ptr(fl), ptr(fc), ptr(a_pre)
+            need = int(lib().moep_predict_split_floats(n, self.H, self.E))
+            scratch = torch.empty(need, dtype=torch.float32, device=self.dev) if need else None
+            A.split_scratch, A.split_scratch_floats = ptr(scratch), need
             check(lib().moep_predict_bf16(A, _stream(self.dev)), "moep_predict_bf16")
             return z, {"a": a_pre}, xb
         x64 = x if x.dtype in (torch.float64, torch.bfloat16) else x.to(torch.float64)

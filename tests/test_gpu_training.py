@@ -235,3 +235,19 @@ def test_dw1_tcgen05_gemm(pb, n, h, d, passes):
     err = float(torch.linalg.vector_norm(out.double() - ref) / torch.linalg.vector_norm(ref))
     assert err < 1e-5, err
     assert float((out.double() - ref).abs().max()) < 1e-4 * float(ref.abs().max()) + 1e-6
+
+
+def test_train_nonfinite_guard_reports_first_step(pb, O):
+    """The reference raises FloatingPointError at the first step whose loss or
+    parameters are non-finite (trainer.py:125-128, 184-187); the device loop
+    keeps a per-step flag and names the same step."""
+    acts, scores, topk = _dataset(O)
+    acts = acts.copy()
+    cfg = pb.TrainConfig(loss=pb.LossSpec(family="wbce"), hidden=32, batch_size=64, epochs=1, seed=5,
+                         eval_fraction=0.2, precision="fp64", learning_rate=1e300)
+    with pytest.raises(FloatingPointError) as e1:
+        pb.train(cfg, pb.TraceFile(16, 8, 2, acts, scores, topk))
+    with pytest.raises(FloatingPointError) as e2:
+        O.train_arch2(acts, scores, topk, 2, hidden=32, batch_size=64, epochs=1, seed=5, eval_fraction=0.2,
+                      loss={"family": "wbce"}, lr=1e300)
+    assert str(e1.value) == str(e2.value)

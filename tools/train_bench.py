@@ -30,10 +30,10 @@ x = torch.randn((n, d), device=dev).to(torch.bfloat16)
 gate = torch.randn((e, d), device=dev) / 64.0
 scores = torch.softmax(x.float() @ gate.T, dim=1).double()
 lab = pb.BatchLabels.from_scores(scores, k)
-dt = torch.float32 if args.precision == "fp32" else torch.float64
+dt = torch.float32 if args.precision in ("fp32", "bf16") else torch.float64
 s_, mk, rk = lab.true_scores.to(dt).contiguous(), lab.topk_mask.to(torch.uint8).contiguous(), lab.rank_of.contiguous()
 tr = pb.DeviceTrainer(m, pb.LossSpec(family="ranking"), "adam", 1e-3, precision=args.precision)
-xin = x if args.precision == "fp32" else x.double()
+xin = x if args.precision in ("fp32", "bf16") else x.double()
 for _ in range(3):
     tr.step(xin, s_, mk, rk)
 torch.cuda.synchronize()
