@@ -172,6 +172,36 @@ class DevicePredictor:
             raise ConfigurationError("input must be finite")
         return x, xb, int(st[1]) == 0
 
+    def topk_speculative(self, x: torch.Tensor, m: int):
+        """The numpy API's path for non-bf16 input (fp64 arrays from the
+        reference): the K0 cast writes bf16(x) and a status (non-finite,
+        not bf16-representable) while K1 + fix-up already run on the cast,
+        all without a host round trip. Returns (ids, cast_status, k1_status);
+        the caller, which synchronises anyway to read the ids, raises on
+        cast_status[0], reruns the exact fp64 path on cast_status[1] (the
+        input was not bf16-representable) and checks k1_status."""
+        if not 1 <= m <= self.E:
+            raise ValueError(f"m={m} out of range for {self.E} experts")
+        x = x.to(self.device)
+        if x.dim() != 2 or x.shape[1] != self.d:
+            raise ConfigurationError(f"input shape {tuple(x.shape)} incompatible with d={self.d}")
+        if x.dtype not in (torch.float64, torch.float32) or not self.k1_usable(True, (m,)) \
+                or x.shape[0] <= self.decode_max_tokens:
+            return None
+        x = x.contiguous()
+        n = x.shape[0]
+        code = MOEP_F64 if x.dtype == torch.float64 else _lib.MOEP_F32
+        xb = torch.empty((n, self.d), dtype=torch.bfloat16, device=self.device)
+        cst = torch.zeros(2, dtype=torch.int32, device=self.device)
+        check(lib().moep_input_norm(ptr(x), code, n, self.d, 0, None, None, 0.0, ptr(xb), ptr(cst),
+                                    _stream(self.device)), "moep_input_norm")
+        ids = torch.empty((n, m), dtype=torch.int32, device=self.device)
+        kst = self.new_status()
+        flags, flist, fcount = self._k1(xb, m_sel=m, bounds=(m,) if m < self.E else (), ids=ids, status=kst)
+        a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, m_sel=m, ids=ids)
+        self._fixup(a, n)
+        return ids, cst, kst
+
     def new_status(self) -> torch.Tensor:
         """A zeroed K1 status word (int32[1]) for the no-sync serving / bench path."""
         return torch.zeros(1, dtype=torch.int32, device=self.device)

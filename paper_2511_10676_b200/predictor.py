@@ -196,7 +196,21 @@ def predict_topk_batch(model: PredictorModel, x, m: int):
     if not 1 <= m <= model.n_experts:
         raise ValueError(f"m={m} out of range for {model.n_experts} experts")
     batch, single, is_t = _as_batch(model, x)
-    ids = device_for(model).topk(batch.to("cuda"), m).to(torch.int64)
+    dev = device_for(model)
+    if not is_t:
+        # numpy input: cast + predict without a host round trip in between; the
+        # status decides after the (unavoidable) read of the ids
+        spec = dev.topk_speculative(batch.to("cuda"), m)
+        if spec is not None:
+            ids, cst, kst = spec
+            ids_np = ids.cpu().numpy().astype(np.int64)
+            st = cst.cpu().numpy()
+            if st[0]:
+                raise ConfigurationError("input must be finite")
+            if st[1] == 0:
+                DevicePredictor.check_status(kst, batch)
+                return ids_np
+    ids = dev.topk(batch.to("cuda"), m).to(torch.int64)
     return ids if is_t else ids.cpu().numpy()
 
 
