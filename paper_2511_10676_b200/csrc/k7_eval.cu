@@ -212,6 +212,149 @@ eval_reg_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict
   }
 }
 
+// v2 (E <= 128): each lane holds EPL CONSECUTIVE experts (e = li * EPL + i:
+// one vector load per lane per token); the stable rank of true expert t is a
+// local count over the lane's slots, summed over the token's lanes with one
+// redux (for 16-lane groups both halves of the warp reduce in the same
+// instruction, packed in 16-bit fields). RPI row groups per warp iteration
+// with every load issued first. ~3x fewer instructions per token than v1.
+template <typename T, int EPL>
+struct VecLoad;
+template <> struct VecLoad<float, 1> { static __device__ void ld(const float* p, float* v) { v[0] = __ldcs(p); } };
+template <> struct VecLoad<float, 2> {
+  static __device__ void ld(const float* p, float* v) { const float2 a = __ldcs(reinterpret_cast<const float2*>(p)); v[0] = a.x; v[1] = a.y; }
+};
+template <> struct VecLoad<float, 4> {
+  static __device__ void ld(const float* p, float* v) {
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(p)); v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  }
+};
+template <> struct VecLoad<double, 1> { static __device__ void ld(const double* p, double* v) { v[0] = __ldcs(p); } };
+template <> struct VecLoad<double, 2> {
+  static __device__ void ld(const double* p, double* v) { const double2 a = __ldcs(reinterpret_cast<const double2*>(p)); v[0] = a.x; v[1] = a.y; }
+};
+template <> struct VecLoad<double, 4> {
+  static __device__ void ld(const double* p, double* v) {
+    const double2 a = __ldcs(reinterpret_cast<const double2*>(p)), b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+};
+
+template <typename T, int LPR, int EPL, int RPI>
+__global__ void __launch_bounds__(NTR)
+eval_v2_kernel(const T* __restrict__ z, int64_t n, int E, const int* __restrict__ truth, int k,
+               int n_m, const int* __restrict__ m_list_dev, int* partials, int n_counters) {
+  constexpr int RPW = 32 / LPR;
+  extern __shared__ int sh[];  // [32 warps][2E] hist
+  __shared__ int scal[NTR / 32][2 + 2 * MOEP_MAX_BOUNDS];
+  __shared__ int mls[MOEP_MAX_BOUNDS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / LPR, li = lane % LPR;
+  const uint32_t submask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  int* hist = sh + warp * 2 * E;
+  for (int i = lane; i < 2 * E; i += 32) hist[i] = 0;
+  if (threadIdx.x < MOEP_MAX_BOUNDS) mls[threadIdx.x] = threadIdx.x < n_m ? m_list_dev[threadIdx.x] : 0;
+  __syncthreads();
+  int m_of[MOEP_MAX_BOUNDS];
+#pragma unroll
+  for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) m_of[mi] = mls[mi];
+  int cnt[2 + 2 * MOEP_MAX_BOUNDS];
+#pragma unroll
+  for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) cnt[i] = 0;
+  const bool full_rows = E == LPR * EPL;  // vector loads need the row to fill the lanes exactly
+  const int e0 = li * EPL;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NTR / 32) + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (NTR / 32);
+  for (int64_t base = gw * RPI * RPW; base < n; base += nw * RPI * RPW) {
+    T zv[RPI][EPL];
+    int tv[RPI];
+#pragma unroll
+    for (int r = 0; r < RPI; ++r) {
+      const int64_t row = base + r * RPW + sub;
+      const bool ok = row < n;
+      if (ok && full_rows) {
+        VecLoad<T, EPL>::ld(z + row * E + e0, zv[r]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) zv[r][i] = (ok && e0 + i < E) ? z[row * E + e0 + i] : T(0);
+      }
+      tv[r] = (ok && li < k) ? __ldcs(truth + row * k + li) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < RPI; ++r) {
+      if (base + r * RPW >= n) break;  // warp-uniform
+      const bool ok = base + r * RPW + sub < n;
+      // experts beyond E (padding) never rank before anything
+#pragma unroll
+      for (int i = 0; i < EPL; ++i)
+        if (e0 + i >= E) zv[r][i] = T(-INFINITY);
+      int my_rank = 0;
+      for (int j = 0; j < k; ++j) {
+        const int t = __shfl_sync(0xffffffffu, tv[r], j, LPR);
+        const int slot = t % EPL;
+        T mine = zv[r][0];
+#pragma unroll
+        for (int i = 1; i < EPL; ++i)
+          if (i == slot) mine = zv[r][i];
+        const T zt = __shfl_sync(0xffffffffu, mine, t / EPL, LPR);
+        uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          const T v = zv[r][i];
+          c += (v > zt || (v == zt && e0 + i < t)) ? 1u : 0u;
+        }
+        uint32_t rk;
+        if (LPR == 16) {
+          const uint32_t tot = __reduce_add_sync(0xffffffffu, c << (16 * sub));
+          rk = (tot >> (16 * sub)) & 0xffffu;
+        } else {
+          rk = __reduce_add_sync(0xffffffffu, c);
+        }
+        if (li == j) my_rank = static_cast<int>(rk);
+      }
+      const bool own = li < k;
+      const int any0 = (__ballot_sync(0xffffffffu, own && my_rank == 0) & submask) != 0;
+      int inside[MOEP_MAX_BOUNDS];
+#pragma unroll
+      for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi)
+        inside[mi] = __popc(__ballot_sync(0xffffffffu, own && my_rank < m_of[mi]) & submask);
+      // shared atomics: a token's true ids may repeat (bincount, metrics.py:182-187)
+      if (ok && own) {
+        atomicAdd(&hist[E + tv[r]], 1);
+        if (my_rank < k) atomicAdd(&hist[tv[r]], 1);
+      }
+      if (ok && li == 0) {
+        cnt[0] += 1;
+        cnt[1] += any0;
+#pragma unroll
+        for (int mi = 0; mi < MOEP_MAX_BOUNDS; ++mi) {
+          cnt[2 + mi] += inside[mi] == k ? 1 : 0;
+          cnt[2 + MOEP_MAX_BOUNDS + mi] += inside[mi];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) cnt[i] = __reduce_add_sync(0xffffffffu, cnt[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 2 + 2 * MOEP_MAX_BOUNDS; ++i) scal[warp][i] = cnt[i];
+  }
+  __syncthreads();
+  int* out = partials + static_cast<int64_t>(blockIdx.x) * n_counters;
+  for (int t = threadIdx.x; t < n_counters; t += NTR) {
+    int v = 0;
+    if (t < 2 + 2 * n_m) {
+      const int src = t < 2 ? t : (t < 2 + n_m ? t : 2 + MOEP_MAX_BOUNDS + (t - 2 - n_m));
+      for (int w = 0; w < NTR / 32; ++w) v += scal[w][src];
+    } else {
+      const int e = t - 2 - 2 * n_m;
+      for (int w = 0; w < NTR / 32; ++w) v += sh[w * 2 * E + e];
+    }
+    out[t] = v;
+  }
+}
+
 // top-m ids (m <= 16) ascending: m rounds of argmax over the token's LPR
 // lanes under the reference key (value, then lower index), then a ballot
 // prefix over expert order. 32 / LPR tokens side by side per warp, RPI groups
@@ -380,9 +523,22 @@ int moep_eval_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, co
       return MOEP_ELAUNCH;                                                                                  \
     kern<<<grid, NTR, smem_r, st>>>(static_cast<const T*>(logits), n, E, truth, k, n_m, m_list, partials, ncnt); \
   } while (0)
+#define MOEP_K7E2(T, LPR, EPL)                                                                              \
+  do {                                                                                                      \
+    auto kern = eval_v2_kernel<T, LPR, EPL, sizeof(T) == 8 ? 2 : 4>;                                                           \
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r) != cudaSuccess) \
+      return MOEP_ELAUNCH;                                                                                  \
+    kern<<<grid, NTR, smem_r, st>>>(static_cast<const T*>(logits), n, E, truth, k, n_m, m_list, partials, ncnt); \
+  } while (0)
+    // v2 (consecutive experts per lane, redux ranks) needs 16-byte aligned rows
+    const bool al = (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
 #define MOEP_K7E_T(T)                                                \
   do {                                                               \
-    if (E <= 16 && k <= 16) MOEP_K7E(T, 16, 1);                      \
+    if (E <= 16 && k <= 16) MOEP_K7E2(T, 16, 1);                     \
+    else if (E <= 32 && k <= 16 && al) MOEP_K7E2(T, 16, 2);          \
+    else if (E <= 64 && k <= 16 && al) MOEP_K7E2(T, 16, 4);          \
+    else if (E <= 128 && al) MOEP_K7E2(T, 32, 4);                    \
+    else if (E <= 16 && k <= 16) MOEP_K7E(T, 16, 1);                 \
     else if (E <= 32 && k <= 16) MOEP_K7E(T, 16, 2);                 \
     else if (E <= 64 && k <= 16) MOEP_K7E(T, 16, 4);                 \
     else if (E <= 32) MOEP_K7E(T, 32, 1);                            \
@@ -395,6 +551,7 @@ int moep_eval_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, co
     else return MOEP_EARG;
 #undef MOEP_K7E_T
 #undef MOEP_K7E
+#undef MOEP_K7E2
     return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
   }
   if (dtype == MOEP_F64) {
