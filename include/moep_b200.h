@@ -90,7 +90,7 @@ typedef struct {
   int32_t kernel;             /* MOEP_K1_AUTO (0) or a forced kernel (tests / measurements) */
 } moep_predict_args;
 
-enum { MOEP_K1_AUTO = 0, MOEP_K1_ONE_SM = 1, MOEP_K1_PAIR_V2 = 2, MOEP_K1_PAIR_V4 = 4 };
+enum { MOEP_K1_AUTO = 0, MOEP_K1_ONE_SM = 1, MOEP_K1_PAIR_V2 = 2, MOEP_K1_PAIR_V4 = 4, MOEP_K1_QUAD_V5 = 5 };
 
 int moep_predict_bf16(const moep_predict_args* a, void* stream);
 

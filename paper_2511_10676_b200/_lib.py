@@ -37,7 +37,7 @@ class PredictArgs(C.Structure):
     ]
 
 
-MOEP_K1_AUTO, MOEP_K1_ONE_SM, MOEP_K1_PAIR_V2, MOEP_K1_PAIR_V4 = 0, 1, 2, 4
+MOEP_K1_AUTO, MOEP_K1_ONE_SM, MOEP_K1_PAIR_V2, MOEP_K1_PAIR_V4, MOEP_K1_QUAD_V5 = 0, 1, 2, 4, 5
 
 
 class Fp64Args(C.Structure):

@@ -556,7 +556,7 @@ extern "C" int moep_predict_bf16(const moep_predict_args* a, void* stream) {
   if (a->arch == 2 && !a->b1) return MOEP_EARG;
   if (a->arch == 1 && (!a->act_alpha || !a->act_beta)) return MOEP_EARG;
   if (a->kernel != MOEP_K1_AUTO && a->kernel != MOEP_K1_ONE_SM && a->kernel != MOEP_K1_PAIR_V2 &&
-      a->kernel != MOEP_K1_PAIR_V4)
+      a->kernel != MOEP_K1_PAIR_V4 && a->kernel != MOEP_K1_QUAD_V5)
     return MOEP_EARG;
   // The CTA-pair kernels (k1v2/k1v4_predict.cu) cover hidden % 256 == 0; the
   // 1-SM kernel below handles every other shape (or kernel == MOEP_K1_ONE_SM).

@@ -710,6 +710,7 @@ extern "C" int64_t moep_predict_split_floats(int64_t n_tokens, int32_t hidden, i
 }
 
 extern "C" int moep_predict_bf16_pair4(const moep_predict_args* a, void* stream);
+extern "C" int moep_predict_bf16_quad5(const moep_predict_args* a, void* stream);
 
 namespace {
 template <int EP, int ARCH>
@@ -749,6 +750,7 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
     p.zpart = a->split_scratch;
     p.zpad = ((a->n_tokens + 2 * BM - 1) / (2 * BM)) * 2 * BM;
   }
+  if (a->kernel == MOEP_K1_QUAD_V5) return moep_predict_bf16_quad5(a, st);
   if (p.split == 1 && use_v4(a) &&
       (a->kernel == MOEP_K1_PAIR_V4 || (a->n_tokens + 2 * BM - 1) / (2 * BM) >= 2 * (grid / 2))) {
     // v4 hides each tile's token epilogue behind the next tile: with fewer

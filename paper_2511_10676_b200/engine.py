@@ -104,6 +104,7 @@ class DevicePredictor:
         self.arch_code = 1 if model.arch == "arch1" else 2
         self.d, self.hidden, self.E = model.d, model.hidden, model.n_experts
         self.tau_abs, self.tau_rel = float(tau_abs), float(tau_rel)
+        self.k1_kernel = _lib.MOEP_K1_AUTO  # forced K1 kernel (tests / A-B timing), else auto
         dev = self.device
         f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
         w1 = f64(model.w1)
@@ -293,7 +294,7 @@ class DevicePredictor:
         need = int(lib().moep_predict_split_floats(n, self.hidden, self.E)) if self.split_hidden else 0
         scratch = torch.empty(need, dtype=torch.float32, device=self.device) if need else None
         a.split_scratch, a.split_scratch_floats = ptr(scratch), need
-        a.status, a.kernel = ptr(status), int(kernel)
+        a.status, a.kernel = ptr(status), int(kernel or self.k1_kernel)
         check(lib().moep_predict_bf16(a, _stream(self.device)), "moep_predict_bf16")
         return flags, flag_list, flag_count
 

@@ -155,12 +155,13 @@ def test_k1_ids_and_counters_vs_oracle(pb, O, arch, d, h, e, k, n):
 
 
 @pytest.mark.parametrize("n,e,kernel", [(16384, 64, 2), (40000, 64, 4), (65536, 128, 4), (40000, 16, 4),
-                                        (4096, 32, 1)])
+                                        (4096, 32, 1), (40000, 64, 5), (30000, 32, 5), (20000, 16, 5)])
 def test_margin_covers_error(pb, O, n, e, kernel):
     """Calibration guard: K1's raw error / row scale stays 8x inside the margin
     (max <= tau/8; tau/2 is the hard limit) on each kernel: v2 (one wave), v4
     (>= 2 tiles per CTA pair; E = 128 has no separate lo accumulator and runs
-    with 1.5 tau) and the 1-SM kernel."""
+    with 1.5 tau), v5 (4-CTA clusters, partial logits of two pairs summed) and
+    the 1-SM kernel."""
     from paper_2511_10676_b200 import _lib
     from paper_2511_10676_b200.engine import TAU_REL
     rng = np.random.default_rng(11 + e)
@@ -314,8 +315,8 @@ def test_large_biases_in_margin(pb, O):
 
 
 def test_forced_kernels_agree(pb, O):
-    """The three K1 kernels (1-SM, pair v2, pair v4; moep_predict_args.kernel)
-    give identical ids on the same input after the fix-up."""
+    """The four K1 kernels (1-SM, pair v2, pair v4, cluster v5;
+    moep_predict_args.kernel) give identical ids on the same input after the fix-up."""
     rng = np.random.default_rng(12)
     n, d, h, e = 40000, 1024, 1024, 64
     m = bf16_model(pb, O, "arch2", d, h, e, seed=12)
@@ -325,7 +326,7 @@ def test_forced_kernels_agree(pb, O):
     dev = m.to_device()
     xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
     from paper_2511_10676_b200.engine import MOEP_BF16
-    for kern in (1, 2, 4):
+    for kern in (1, 2, 4, 5):
         ids = torch.empty((n, 6), dtype=torch.int32, device="cuda")
         flags, flist, fcount = dev._k1(xt, m_sel=6, bounds=(6,), ids=ids, kernel=kern)
         a = dev._fp64_args(xt, MOEP_BF16, rows=flist, row_count=fcount, m_sel=6, ids=ids)
@@ -462,3 +463,31 @@ def test_ties_through_hidden_split_and_decode(pb, O):
         xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
         for mm in (1, 2, 3, 5):
             assert np.array_equal(dev.topk(xt, mm).cpu().numpy(), O.top_k_batch(zref, mm)), (n, mm)
+
+
+@pytest.mark.parametrize("n,e,arch", [(40000, 64, "arch2"), (33000, 32, "arch1"), (300, 64, "arch2"),
+                                      (70001, 16, "arch2")])
+def test_v5_cluster_kernel_evaluate(pb, O, n, e, arch):
+    """K1 v5 (two CTA pairs per 256-token tile, x multicast, partial logits
+    exchanged through distributed shared memory) through the full evaluate
+    pipeline: ids and every counter equal the oracle's, including a ragged last
+    tile, fewer tiles than clusters (n = 300) and arch1's activation."""
+    rng = np.random.default_rng(n + e)
+    d, h = 1024, 1536
+    m = bf16_model(pb, O, arch, d, h, e, seed=9)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref = O.predict_logits(oracle_params(m), x)
+    truth = O.top_k_batch(zref + 0.05 * rng.standard_normal(zref.shape), 6)
+    dev = m.to_device()
+    dev.k1_kernel = 5
+    dev.decode_max_tokens = 0
+    ms = [6, 10, e]
+    cnt, fc, ids = dev.evaluate(torch.from_numpy(x).to("cuda", torch.bfloat16), torch.from_numpy(truth), 6, ms,
+                                ids_m=6)
+    assert np.array_equal(ids.cpu().numpy(), O.top_k_batch(zref, 6))
+    c = pb.EvalCounters.from_array(cnt.cpu().numpy(), 6, e, ms)
+    oc = O.eval_counters(zref, truth, e, ms)
+    assert c.n == oc["n"] and c.top1 == oc["top1_count"]
+    assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
+    assert np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
+    assert np.array_equal(c.per_expert_truth, oc["per_expert_truth"])

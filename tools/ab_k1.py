@@ -3,7 +3,7 @@ builds (tools/variant_lib.py) are loaded side by side (ctypes RTLD_LOCAL) and
 timed round-robin on the same 1M-token DSV2L layer, so clock / power drift
 hits every variant alike.
 
-    python tools/ab_k1.py tools/_variants/zlo/libmoep_b200.so [...] [--rounds 6] [--kind gate]
+    python tools/ab_k1.py tools/_variants/zlo/libmoep_b200.so [...] [--rounds 6] [--kind gate] [--kernels 4,5]
 """
 import argparse
 import ctypes as C
@@ -36,18 +36,22 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--kind", default="gate")
     ap.add_argument("--E", type=int, default=64)
+    ap.add_argument("--kernels", default="0", help="comma list of moep_predict_args.kernel values (0 = auto)")
     args = ap.parse_args()
     dev = torch.device("cuda")
+    kernels = [int(v) for v in args.kernels.split(",")]
     libs = [("product", _lib.lib())] + [(p, load(p)) for p in args.libs]
+    libs = [(f"{n} k{kv}", L, kv) for n, L in libs for kv in kernels]
     k = 6 if args.E == 64 else 8
     model, x, truth = W.make_layer(args.kind, 2048, 2048, args.E, k, 1 << 20, seed=1, device=dev)
     dp = pb.DevicePredictor(model, dev)
     part = torch.empty((dp.n_sms, 2 + 6 + 2 * args.E), dtype=torch.int32, device=dev)
     ms_list = [k, k + 4, args.E]
-    res = {n: [] for n, _ in libs}
+    res = {n: [] for n, _, _ in libs}
     for r in range(args.rounds):
-        for name, L in libs:
+        for name, L, kv in libs:
             _lib._lib = L
+            dp.k1_kernel = kv
             run = lambda: dp._k1(x, m_sel=k, bounds=(1, k, k + 4), ids=torch.empty((x.shape[0], k), dtype=torch.int32,
                                                                                    device=dev),
                                  truth=truth, k=k, m_values=ms_list, partials=part)
