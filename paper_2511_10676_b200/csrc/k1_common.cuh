@@ -38,9 +38,39 @@ struct Params {
 };
 
 // mbarrier wait that traps instead of hanging forever (a lost arrival becomes a
-// launch error, not a wedged GPU).
+// launch error, not a wedged GPU). try_wait carries a suspend-time hint: the
+// warp sleeps until the phase completes (or the hint expires) instead of
+// re-issuing the probe every ~30 cycles. Without it the spin loops of the
+// TMA / MMA / epilogue waits were 35 % of the instructions K1 v4 issued (ncu
+// per-instruction counts), taking issue slots from the epilogue warps on the
+// same SM sub-partitions. A wait still pending after 20 s of %globaltimer traps.
+#ifndef MOEP_WAIT_HINT_NS
+#define MOEP_WAIT_HINT_NS 0x989680
+#endif
 __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0, spins = 0;
+  uint32_t done = 0;
+#if MOEP_WAIT_HINT_NS > 0
+  uint64_t t0 = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(MOEP_WAIT_HINT_NS)
+        : "memory");
+    if (done) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t0 == 0) {
+      t0 = t;
+    } else if (t - t0 > 20000000000ull) {
+      printf("moep k1: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+      asm volatile("trap;");
+    }
+  }
+#else
+  uint32_t spins = 0;
   while (true) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
@@ -55,6 +85,7 @@ __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
       asm volatile("trap;");
     }
   }
+#endif
 }
 
 // non-blocking probe of an mbarrier phase

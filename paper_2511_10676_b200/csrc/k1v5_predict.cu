@@ -132,17 +132,22 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
 }
 // wait with acquire at cluster scope (data written by the peer CTA)
 __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0, spins = 0;
+  uint32_t done = 0;
+  uint64_t t0 = 0;
   while (true) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, P1;\n\t}"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680)
         : "memory");
     if (done) return;
-    if (++spins == (1u << 26)) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t0 == 0) {
+      t0 = t;
+    } else if (t - t0 > 20000000000ull) {
       printf("moep k1v5: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
       asm volatile("trap;");
     }
