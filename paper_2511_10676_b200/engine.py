@@ -31,11 +31,15 @@ K1_MAX_SEL = 15       # K1 keeps 16 sorted positions per token
 K1_MAX_EXPERTS = 128  # TMEM budget of the single-CTA kernel
 TAU_ABS = 1e-7
 # Every logit must lie within delta/2 of its exact value. Measured max
-# |dz| / (||h|| max||w2_e||) of K1 over 1M-token DSV2L layers: 6.2e-7 with the
-# separate lo-product accumulator (tools/precision_scan.py), so
-# tau_rel = 5e-6 leaves 8x headroom (max <= tau_rel / 8); bench.py re-measures
-# the max over every checked token of the run.
-TAU_REL = 5e-6
+# |dz| / (||h|| max||w2_e||) of K1 over every kernel and workload
+# (tools/margin_ratios.py, tools/precision_scan.py; 1M-token DSV2L / Qwen3
+# layers, random init and oracle-gate): 6.5e-7 (kernels without the separate
+# lo accumulator run at 1.5 tau: 9.2e-7 / 1.5). tau_rel = 3e-6 is 4.6x the
+# worst observed error (the hard limit tau_rel / 2 is 2.3x it); the guard
+# tests hold every kernel to max <= tau / 4 and bench.py re-measures the max
+# over every checked token of the run. From 5e-6 (8x) the flagged fraction
+# of the bench workload fell 0.245 % -> 0.146 %.
+TAU_REL = 3e-6
 DECODE_MAX_TOKENS = 64  # batches up to this size take the split-hidden exact fp64 decode kernel
 
 

@@ -157,8 +157,8 @@ def test_k1_ids_and_counters_vs_oracle(pb, O, arch, d, h, e, k, n):
 @pytest.mark.parametrize("n,e,kernel", [(16384, 64, 2), (40000, 64, 4), (65536, 128, 4), (40000, 16, 4),
                                         (4096, 32, 1), (40000, 64, 5), (30000, 32, 5), (20000, 16, 5)])
 def test_margin_covers_error(pb, O, n, e, kernel):
-    """Calibration guard: K1's raw error / row scale stays 8x inside the margin
-    (max <= tau/8; tau/2 is the hard limit) on each kernel: v2 (one wave), v4
+    """Calibration guard: K1's raw error / row scale stays 4x inside the margin
+    (max <= tau/4; tau/2 is the hard limit) on each kernel: v2 (one wave), v4
     (>= 2 tiles per CTA pair; E = 128 has no separate lo accumulator and runs
     with 1.5 tau), v5 (4-CTA clusters, partial logits of two pairs summed) and
     the 1-SM kernel."""
@@ -178,7 +178,7 @@ def test_margin_covers_error(pb, O, n, e, kernel):
     scale = np.linalg.norm(cache["h"], axis=1) * np.linalg.norm(m.w2, axis=1).max()
     ratio = err / scale
     tau = TAU_REL * (1.5 if (kernel == 4 and e > 64) or kernel == 1 else 1.0)
-    assert 8 * ratio.max() <= tau, (ratio.max(), tau)
+    assert 4 * ratio.max() <= tau, (ratio.max(), tau)
 
 
 @pytest.mark.parametrize("n,e", [(256, 64), (4096, 64), (8192, 128), (300, 16)])
@@ -200,7 +200,7 @@ def test_margin_covers_error_hidden_split(pb, O, n, e):
     dev._k1(xt, logits=lg)
     err = np.abs(lg.double().cpu().numpy() - zref).max(axis=1)
     scale = np.linalg.norm(cache["h"], axis=1) * np.linalg.norm(m.w2, axis=1).max()
-    assert 8 * (err / scale).max() <= TAU_REL, (err / scale).max()
+    assert 4 * (err / scale).max() <= TAU_REL, (err / scale).max()
     dev.decode_max_tokens = 0
     ids_split = dev.topk(xt, 6).cpu().numpy()
     dev.split_hidden = False
