@@ -80,22 +80,38 @@ __device__ __forceinline__ uint32_t special2(uint32_t w) {
   return ((ex + 0x00800080u) | (ex - 0x00800080u)) & 0x80008000u;
 }
 
-// rmsnorm: x*x is exact in fp32 for bf16 x with exponent field in [64, 190];
-// flags either half outside that range (or zero / subnormal / inf / nan)
-__device__ __forceinline__ uint32_t special2_sq(uint32_t w) {
-  const uint32_t ex = w & 0x7f807f80u;
-  return ((ex + 0x20802080u) | (ex - 0x20002000u)) & 0x80008000u;
+// |bf16| -> fp64 by integer ops (sign dropped: the operand of a square)
+__device__ __forceinline__ double bf16lo_abs_f64(uint32_t w) {
+  return __hiloint2double(static_cast<int>((w & 0x7fffu) * 8192u + 0x38000000u), 0);
 }
-// positive normal fp32 -> fp64 by integer ops
-__device__ __forceinline__ double f32pos_f64_fast(float f) {
-  const uint32_t u = __float_as_uint(f);
-  return __hiloint2double(static_cast<int>((u >> 3) + 0x38000000u), static_cast<int>(u << 29));
+__device__ __forceinline__ double bf16hi_abs_f64(uint32_t w) {
+  return __hiloint2double(static_cast<int>(((w & 0x7fff0000u) >> 3) + 0x38000000u), 0);
+}
+// packed fp32x2 arithmetic (sm_100: one instruction per pair, round to nearest)
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
 }
 
 // KIND 1 rmsnorm, 2 layernorm. B lanes per row, 32 / B rows per warp. Each
 // lane stages its leaf (256 B, padded to 272 B so a quarter-warp's 16-byte
-// shared loads hit distinct banks) and re-reads only its own staging: no
-// barrier inside the row loop.
+// shared loads hit distinct banks; an XOR swizzle without the pad measured 5 %
+// slower on layernorm) and re-reads only its own staging: no barrier inside
+// the row loop. Shared memory holds only the gamma / beta rows the kernel uses.
 //
 // Statistics: numpy's order in fp64 (bit-identical mean / var by
 // construction). Output, level 1: fp32 arithmetic with the fp32-rounded
@@ -105,12 +121,12 @@ __device__ __forceinline__ double f32pos_f64_fast(float f) {
 // when no bf16 rounding midpoint lies within E of res32 (and res32 is in the
 // bf16 normal range, E < 2^-10 |res|), bf16_rn(res32) == bf16_rn(numpy's).
 // Level 2 (~1 element in 4000): numpy's fp64 chain with the exact statistics.
-constexpr int kStageU4 = 17;
+constexpr int kStageU4 = 17;  // per-lane leaf staging: 16 chunks + 1 pad (bank-conflict-free quarter warps)
 constexpr int kNormThreads = 256;
 
 
 template <int B, int KIND, bool GAMMA, bool BETA, bool FORCE = false>
-__global__ void __launch_bounds__(kNormThreads)
+__global__ void __launch_bounds__(kNormThreads, 2)  // 128 registers: two blocks per SM (three spill)
 norm_fast_kernel(const uint16_t* __restrict__ x, int64_t n, const double* __restrict__ gamma,
                  const double* __restrict__ beta, double eps, uint16_t* __restrict__ out, int* status) {
   constexpr int RPW = 32 / B;
@@ -123,11 +139,12 @@ norm_fast_kernel(const uint16_t* __restrict__ x, int64_t n, const double* __rest
   extern __shared__ __align__(16) float sg32[];
   for (int i = threadIdx.x; i < D; i += blockDim.x) {
     if (GAMMA) sg32[(i >> 7) * GP + (i & 127)] = static_cast<float>(gamma[i]);
-    if (BETA) sg32[B * GP + (i >> 7) * GP + (i & 127)] = static_cast<float>(beta[i]);
+    if (BETA) sg32[(GAMMA ? B * GP : 0) + (i >> 7) * GP + (i & 127)] = static_cast<float>(beta[i]);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, sub = lane / B, li = lane % B;
-  uint4* const stage = reinterpret_cast<uint4*>(sg32 + 2 * B * GP) + (threadIdx.x >> 5) * 32 * kStageU4;
+  constexpr int NREG = (GAMMA ? 1 : 0) + (BETA ? 1 : 0);  // gamma / beta rows present
+  uint4* const stage = reinterpret_cast<uint4*>(sg32 + NREG * B * GP) + (threadIdx.x >> 5) * 32 * kStageU4;
   uint4* const my = stage + lane * kStageU4;
   const int64_t wg = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -135,31 +152,35 @@ norm_fast_kernel(const uint16_t* __restrict__ x, int64_t n, const double* __rest
   const double* gl = GAMMA ? gamma + 128 * li : nullptr;
   const double* bl = BETA ? beta + 128 * li : nullptr;
   const float4* gl32 = reinterpret_cast<const float4*>(sg32 + GP * li);
-  const float4* bl32 = reinterpret_cast<const float4*>(sg32 + B * GP + GP * li);
+  const float4* bl32 = reinterpret_cast<const float4*>(sg32 + (GAMMA ? B * GP : 0) + GP * li);
   const unsigned grp = (B == 32) ? 0xffffffffu : (((1u << B) - 1u) << (sub * B));
+  uint4 v[16];
+  auto fetch = [&](int64_t rs) {
+    const int64_t rh = n - rs < RPW ? n - rs : RPW;
+    const uint4* src = reinterpret_cast<const uint4*>(x + rs * D);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int idx = t * 32 + lane;
+      v[t] = (rs < n && idx / (D / 8) < rh) ? __ldcs(src + idx) : make_uint4(0, 0, 0, 0);
+    }
+  };
   for (int64_t r0 = wg * RPW; r0 < n; r0 += nw * RPW) {
     const int64_t row = r0 + sub;
     const bool valid = row < n;
     // the warp's RPW consecutive rows are one contiguous 8 KB piece: coalesced
     // 16-byte loads into the owners' staging (chunk q of a row -> leaf q / 16).
-    // (A double-buffered cp.async variant, 4 warps per block, measured slower:
-    // 2.95 vs 2.16 ms per 1M x 2048 rmsnorm — the kernel is issue-bound.)
+    // (Measured slower: a double-buffered cp.async variant with 4 warps per
+    // block, 2.95 vs 2.16 ms per 1M x 2048 rmsnorm, and a register double
+    // buffer of the next row group, 2.36 ms at 128 registers (spills) / 2.77 ms
+    // at one block per SM, against 2.12 ms.)
     const int64_t rows_here = n - r0 < RPW ? n - r0 : RPW;
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(x + r0 * D);
-      uint4 v[16];
+    fetch(r0);
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int idx = t * 32 + lane;
-        v[t] = idx / (D / 8) < rows_here ? __ldcs(src + idx) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int idx = t * 32 + lane;
-        stage[(idx >> 4) * kStageU4 + (idx & 15)] = v[t];  // owner lane = row * B + leaf = idx / 16
-      }
-      __syncwarp();
+    for (int t = 0; t < 16; ++t) {
+      const int idx = t * 32 + lane;
+      stage[(idx >> 4) * kStageU4 + (idx & 15)] = v[t];  // owner lane = row * B + leaf = idx / 16
     }
+    __syncwarp();
     // leaf sum of op(x) in numpy's order: r[j] starts at element j, then += element 8c + j
     uint32_t spec = 0;
     auto leaf_fast = [&](auto op) -> double {
@@ -179,21 +200,26 @@ norm_fast_kernel(const uint16_t* __restrict__ x, int64_t n, const double* __rest
       return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
     };
-    auto leaf_sq_fast = [&]() -> double {  // rmsnorm: fp32 squares (exact), then fp64 in numpy's order
+    auto leaf_sq_fast = [&]() -> double {
+      // rmsnorm: x*x is exact in fp64 (8-bit mantissas), so fma(x, x, r) rounds
+      // once exactly like numpy's r + (x*x); the zero / subnormal / inf / nan
+      // test is OR-accumulated and masked once per leaf
       double r[8];
+      uint32_t sp = 0;
 #pragma unroll 4
       for (int c = 0; c < 16; ++c) {
         const uint4 q = my[c];
 #pragma unroll
         for (int j2 = 0; j2 < 4; ++j2) {
           const uint32_t w = word8(q, j2);
-          spec |= special2_sq(w);
-          const float a = __uint_as_float(w << 16), b = __uint_as_float(w & 0xffff0000u);
-          const double e0 = f32pos_f64_fast(__fmul_rn(a, a)), e1 = f32pos_f64_fast(__fmul_rn(b, b));
-          if (c == 0) { r[2 * j2] = e0; r[2 * j2 + 1] = e1; }
-          else { r[2 * j2] = __dadd_rn(r[2 * j2], e0); r[2 * j2 + 1] = __dadd_rn(r[2 * j2 + 1], e1); }
+          const uint32_t ex = w & 0x7f807f80u;
+          sp |= (ex + 0x00800080u) | (ex - 0x00800080u);
+          const double e0 = bf16lo_abs_f64(w), e1 = bf16hi_abs_f64(w);
+          if (c == 0) { r[2 * j2] = __dmul_rn(e0, e0); r[2 * j2 + 1] = __dmul_rn(e1, e1); }
+          else { r[2 * j2] = __fma_rn(e0, e0, r[2 * j2]); r[2 * j2 + 1] = __fma_rn(e1, e1, r[2 * j2 + 1]); }
         }
       }
+      spec |= sp & 0x80008000u;
       return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
     };
@@ -260,14 +286,17 @@ norm_fast_kernel(const uint16_t* __restrict__ x, int64_t n, const double* __rest
         const uint32_t w = word8(q, j2);
         float resv[2];
         bool amb[2];
+        // the pair (lo, hi) in packed fp32x2 ops: same RN results as the scalar chain
+        const float2 x2 = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+        const float2 dl2 = KIND == 2 ? sub2(x2, make_float2(mu32, mu32)) : x2;
+        const float2 y2 = mul2(dl2, make_float2(r32, r32));
+        const float2 g2 = GAMMA ? mul2(y2, make_float2(gv[2 * j2], gv[2 * j2 + 1])) : y2;
+        const float2 res2 = BETA ? add2(g2, make_float2(bv[2 * j2], bv[2 * j2 + 1])) : g2;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float xf = __uint_as_float(h ? (w & 0xffff0000u) : (w << 16));
-          const float dl = KIND == 2 ? __fsub_rn(xf, mu32) : xf;
-          const float y = __fmul_rn(dl, r32);
+          const float dl = h ? dl2.y : dl2.x;
           const float gm = GAMMA ? gv[2 * j2 + h] : 1.0f;
-          const float g = GAMMA ? __fmul_rn(y, gm) : y;
-          const float res = BETA ? __fadd_rn(g, bv[2 * j2 + h]) : g;
+          const float res = h ? res2.y : res2.x;
           const uint32_t rb = __float_as_uint(res);
           const uint32_t ex = (rb >> 23) & 0xffu;
           bool a;
@@ -313,7 +342,8 @@ norm_fast_kernel(const uint16_t* __restrict__ x, int64_t n, const double* __rest
 #pragma unroll
       for (int t = 0; t < 16; ++t) {
         const int idx = t * 32 + lane;
-        if (idx / (D / 8) < rows_here) __stcs(dst + idx, stage[(idx >> 4) * kStageU4 + (idx & 15)]);
+        if (idx / (D / 8) < rows_here)
+          __stcs(dst + idx, stage[(idx >> 4) * kStageU4 + (idx & 15)]);
       }
       __syncwarp();
     }
@@ -412,9 +442,9 @@ int launch_fast(const uint16_t* x, int64_t n, int kind, bool force, const double
   const int threads = kNormThreads;
   const int rows_per_block = (threads / 32) * (32 / B);
   const int64_t want = (n + rows_per_block - 1) / rows_per_block;
-  const size_t sm = static_cast<size_t>(2 * 132 * B) * sizeof(float) + (threads / 32) * 32 * kStageU4 * 16;
   int rc = MOEP_OK;
-  auto go = [&](auto kern) {
+  auto go = [&](auto kern, int nreg) {
+    const size_t sm = static_cast<size_t>(nreg * 132 * B) * sizeof(float) + (threads / 32) * 32 * kStageU4 * 16;
     // one resident wave (grid-stride over row groups): blocks per SM from the
     // occupancy calculator, cached per (kernel, device)
     int dev = 0;
@@ -441,19 +471,19 @@ int launch_fast(const uint16_t* x, int64_t n, int kind, bool force, const double
     }
   };
   if (force) {  // tests: numpy's exact chain for every element (checks the fast path's rounding decision)
-    if (kind == 1) go(norm_fast_kernel<B, 1, true, false, true>);
-    else go(norm_fast_kernel<B, 2, true, true, true>);
+    if (kind == 1) go(norm_fast_kernel<B, 1, true, false, true>, 1);
+    else go(norm_fast_kernel<B, 2, true, true, true>, 2);
   } else if (kind == 1) {
-    if (gamma) go(norm_fast_kernel<B, 1, true, false>);
-    else go(norm_fast_kernel<B, 1, false, false>);
+    if (gamma) go(norm_fast_kernel<B, 1, true, false>, 1);
+    else go(norm_fast_kernel<B, 1, false, false>, 0);
   } else if (gamma && beta) {
-    go(norm_fast_kernel<B, 2, true, true>);
+    go(norm_fast_kernel<B, 2, true, true>, 2);
   } else if (gamma) {
-    go(norm_fast_kernel<B, 2, true, false>);
+    go(norm_fast_kernel<B, 2, true, false>, 1);
   } else if (beta) {
-    go(norm_fast_kernel<B, 2, false, true>);
+    go(norm_fast_kernel<B, 2, false, true>, 1);
   } else {
-    go(norm_fast_kernel<B, 2, false, false>);
+    go(norm_fast_kernel<B, 2, false, false>, 0);
   }
   return rc;
 }
