@@ -405,20 +405,64 @@ def check_parity(layers, outs, flat_np, args, world, n_sample=1 << 16, n_oracle=
     return res
 
 
+def _reference_package():
+    """The unmodified reference (moepredict, installed offline into
+    baseline/_ref): (predictor, core, metrics) modules, or None when absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "moepredict")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import moepredict.core as C
+        import moepredict.metrics as M
+        import moepredict.predictor as P
+    except Exception:  # noqa: BLE001 - a broken install falls back to the port
+        return None
+    return P, C, M
+
+
+def _ref_model(P, w1, b1, w2, b2):
+    m = P.init_model("arch2", w1.shape[1], w1.shape[0], w2.shape[0], seed=0)
+    m.w1, m.b1, m.w2, m.b2 = (np.asarray(a, dtype=np.float64).copy() for a in (w1, b1, w2, b2))
+    return m.eval()
+
+
+def _ref_step(pkg, model, x, truth):
+    """predict_logits + top_k_batch + evaluate_predictions: the reference
+    package when present (kind "reference"), else the oracle port."""
+    if pkg is not None:
+        P, C, M = pkg
+        z = P.predict_logits(model, x)
+        C.top_k_batch(z, K_ACT)
+        M.evaluate_predictions(z, truth, E, M_LIST)
+    else:
+        from oracle import oracle as O
+        z = O.predict_logits(model, x)
+        O.top_k_batch(z, K_ACT)
+        O.evaluate_predictions(z, truth, E, M_LIST)
+
+
 def cpu_baseline(model, x, truth, n_sample=32768):
-    """The oracle port (numpy fp64, all host threads) on a bounded sample."""
-    from oracle import oracle as O
+    """The reference's own CPU path (moepredict from baseline/_ref, numpy fp64,
+    all host threads; the oracle port when the package is absent) on a bounded
+    sample of layer 0."""
+    pkg = _reference_package()
     xs = x[:n_sample].float().cpu().numpy().astype(np.float64)
     tr = truth[:n_sample].cpu().numpy().astype(np.int64)
-    p = {"arch": "arch2", "w1": model.w1, "b1": model.b1, "w2": model.w2, "b2": model.b2}
+    if pkg is not None:
+        ref = _ref_model(pkg[0], model.w1, model.b1, model.w2, model.b2)
+        what = "moepredict 0.1.0 (baseline/_ref, unmodified)"
+    else:
+        ref = {"arch": "arch2", "w1": model.w1, "b1": model.b1, "w2": model.w2, "b2": model.b2}
+        what = "oracle/oracle.py port"
     t0 = time.perf_counter()
-    z = O.predict_logits(p, xs)
-    O.top_k_batch(z, K_ACT)
-    O.evaluate_predictions(z, tr, E, M_LIST)
+    _ref_step(pkg, ref, xs, tr)
     dt = time.perf_counter() - t0
-    return {"value": n_sample / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+    return {"value": n_sample / dt, "unit": "tokens/s", "cores": os.cpu_count(),
+            "kind": "reference" if pkg is not None else "port",
             "sample": f"{n_sample} tokens of layer 0: predict_logits + top_k_batch(6) + evaluate_predictions "
-                      f"(oracle/oracle.py numpy fp64, OpenBLAS all threads), {dt:.2f} s"}
+                      f"({what}, numpy fp64, OpenBLAS all threads), {dt:.2f} s"}
 
 
 def deploy_arm(layer, dev, reps=5):
@@ -795,24 +839,36 @@ def train_arm(args, rank, world, dev, n_local=16384, steps=10):
 
 # ------------------------------------------------------------- reference arm
 def reference_arm(args, rank, world):
-    """The reference's CPU implementation of the path (the oracle port:
-    oracle/oracle.py restates moepredict's float64 numpy code) on the host cores,
-    on a bounded sample of the same workload per step. Rank 0 only."""
+    """The reference's CPU implementation of the path on the host cores, on a
+    bounded sample of the same workload per step: the unmodified moepredict
+    package from baseline/_ref (predictor.predict_logits, core.top_k_batch,
+    metrics.evaluate_predictions), or the oracle port when it is absent.
+    Rank 0 only."""
     if rank != 0:
         return
-    from oracle import oracle as O
+    pkg = _reference_package()
     rng = np.random.default_rng(0)
     n = 8192
-    p = O.init_params("arch2", D, H, E, seed=0)
-    p["w1"], p["w2"] = O.round_bf16(p["w1"]), O.round_bf16(p["w2"])
-    x = O.round_bf16(rng.standard_normal((n, D)))
+
+    def bf(a):
+        m, e = np.frexp(np.asarray(a, dtype=np.float64))
+        return np.ldexp(np.rint(m * 256.0), e - 8)
+    x = bf(rng.standard_normal((n, D)))
     gate = rng.standard_normal((E, D)) / np.sqrt(D)
-    truth = O.top_k_batch(O.layer_norm(x) @ gate.T, K_ACT)
+    xn = (x - x.mean(1, keepdims=True)) / np.sqrt(x.var(1, keepdims=True) + 1e-5)
+    truth = np.argsort(-(xn @ gate.T), axis=1, kind="stable")[:, :K_ACT]
+    if pkg is not None:
+        m0 = pkg[0].init_model("arch2", D, H, E, seed=0)
+        model = _ref_model(pkg[0], bf(m0.w1), m0.b1, bf(m0.w2), m0.b2)
+        what = "moepredict 0.1.0 (baseline/_ref, unmodified)"
+    else:
+        from oracle import oracle as O
+        p = O.init_params("arch2", D, H, E, seed=0)
+        model = dict(p, w1=bf(p["w1"]), w2=bf(p["w2"]))
+        what = "oracle/oracle.py port"
 
     def one():
-        z = O.predict_logits(p, x)
-        O.top_k_batch(z, K_ACT)
-        O.evaluate_predictions(z, truth, E, M_LIST)
+        _ref_step(pkg, model, x, truth)
     for _ in range(max(1, min(args.warmup, 1))):
         one()
     t0 = time.perf_counter()
@@ -827,9 +883,10 @@ def reference_arm(args, rank, world):
         "config": {"workload": "DeepSeek-V2-Lite all MoE layers: predictor inference + top-6 accuracy eval "
                                "(BASELINE configs[1]); each step is a bounded sample of one layer",
                    "tokens_per_step": n, "d": D, "hidden": H, "experts": E, "k": K_ACT, "m_list": M_LIST},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(),
+                         "kind": "reference" if pkg is not None else "port",
                          "sample": f"{n} tokens x {args.steps} steps: predict_logits + top_k_batch + "
-                                   "evaluate_predictions, numpy fp64 / OpenBLAS all threads"},
+                                   f"evaluate_predictions ({what}), numpy fp64 / OpenBLAS all threads"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
