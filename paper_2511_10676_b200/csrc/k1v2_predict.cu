@@ -751,6 +751,14 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
     p.zpad = ((a->n_tokens + 2 * BM - 1) / (2 * BM)) * 2 * BM;
   }
   if (a->kernel == MOEP_K1_QUAD_V5) return moep_predict_bf16_quad5(a, st);
+  // One wave of unsplit tiles with d >= 4096: the pairs' live x tiles (2 MB
+  // each) overflow L2 and every hidden chunk re-reads them from DRAM; the
+  // 4-CTA cluster kernel shares each tile between two pairs (TMA multicast)
+  // and halves the live set. Phi-shape training forward (16 k tokens, d = 4096,
+  // E = 16): 0.258 -> 0.227 ms (tools/ab_k1.py).
+  if (a->kernel == MOEP_K1_AUTO && p.split == 1 && a->n_experts <= 64 && a->hidden % 512 == 0 && a->d >= 4096 &&
+      (a->n_tokens + 2 * BM - 1) / (2 * BM) < grid / 2)
+    return moep_predict_bf16_quad5(a, st);
   if (p.split == 1 && use_v4(a) &&
       (a->kernel == MOEP_K1_PAIR_V4 || (a->n_tokens + 2 * BM - 1) / (2 * BM) >= 2 * (grid / 2))) {
     // v4 hides each tile's token epilogue behind the next tile: with fewer

@@ -55,6 +55,7 @@ class DeviceTrainer:
         self.loss_spec, self.kind = loss, OPT_KIND[optimizer]
         self.lr, self.momentum, self.beta1, self.beta2, self.eps = lr, momentum, beta1, beta2, eps
         self.precision = precision
+        self.k1_kernel = _lib.MOEP_K1_AUTO  # forced forward K1 kernel (A-B timing), else auto
         self.dt = torch.float64 if precision == "fp64" else torch.float32
         self.d, self.H, self.E = model.d, model.hidden, model.n_experts
         d, H, E = self.d, self.H, self.E
@@ -133,6 +134,7 @@ class DeviceTrainer:
             need = int(lib().moep_predict_split_floats(n, self.H, self.E))
             scratch = torch.empty(need, dtype=torch.float32, device=self.dev) if need else None
             A.split_scratch, A.split_scratch_floats = ptr(scratch), need
+            A.kernel = int(self.k1_kernel)
             check(lib().moep_predict_bf16(A, _stream(self.dev)), "moep_predict_bf16")
             return z, {"a": a_pre}, xb
         x64 = x if x.dtype in (torch.float64, torch.bfloat16) else x.to(torch.float64)

@@ -36,14 +36,16 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--kind", default="gate")
     ap.add_argument("--E", type=int, default=64)
+    ap.add_argument("--d", type=int, default=2048)
+    ap.add_argument("--n", type=int, default=1 << 20)
     ap.add_argument("--kernels", default="0", help="comma list of moep_predict_args.kernel values (0 = auto)")
     args = ap.parse_args()
     dev = torch.device("cuda")
     kernels = [int(v) for v in args.kernels.split(",")]
     libs = [("product", _lib.lib())] + [(p, load(p)) for p in args.libs]
     libs = [(f"{n} k{kv}", L, kv) for n, L in libs for kv in kernels]
-    k = 6 if args.E == 64 else 8
-    model, x, truth = W.make_layer(args.kind, 2048, 2048, args.E, k, 1 << 20, seed=1, device=dev)
+    k = 6 if args.E == 64 else (2 if args.E == 16 else 8)
+    model, x, truth = W.make_layer(args.kind, args.d, 2048, args.E, k, args.n, seed=1, device=dev)
     dp = pb.DevicePredictor(model, dev)
     part = torch.empty((dp.n_sms, 2 + 6 + 2 * args.E), dtype=torch.int32, device=dev)
     ms_list = [k, k + 4, args.E]

@@ -20,6 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=4096)
 ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--precision", default="fp32")
+ap.add_argument("--k1-kernel", type=int, default=0, help="forced forward K1 kernel (moep_predict_args.kernel)")
 args = ap.parse_args()
 d, h, e, k, n = 4096, 2048, 16, 2, args.batch
 rng = np.random.default_rng(0)
@@ -33,6 +34,7 @@ lab = pb.BatchLabels.from_scores(scores, k)
 dt = torch.float32 if args.precision in ("fp32", "bf16") else torch.float64
 s_, mk, rk = lab.true_scores.to(dt).contiguous(), lab.topk_mask.to(torch.uint8).contiguous(), lab.rank_of.contiguous()
 tr = pb.DeviceTrainer(m, pb.LossSpec(family="ranking"), "adam", 1e-3, precision=args.precision)
+tr.k1_kernel = args.k1_kernel
 xin = x if args.precision in ("fp32", "bf16") else x.double()
 for _ in range(3):
     tr.step(xin, s_, mk, rk)
