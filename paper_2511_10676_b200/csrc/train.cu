@@ -719,6 +719,29 @@ static void sum_parts3(const T* dw2_part, const T* db1_part, const T* db2_part, 
 // Operation order follows trainer.py:109-122 (m *= b1; m += (1-b1) g; ...),
 // evaluated in T (fp64 for the exact-parity mode, fp32 master otherwise).
 template <typename T>
+__device__ __forceinline__ T optim_elem(T pi, T gi, T* mi_io, T* vi_io, int kind, T lr, T b1, T b2, T eps, T bc1,
+                                       T bc2, T mom) {
+  if (kind == 0) {          // sgd
+    pi -= lr * gi;
+  } else if (kind == 1) {   // momentum: m = mu*m + g ; p -= lr*m
+    T mi = *mi_io * mom;
+    mi += gi;
+    *mi_io = mi;
+    pi -= lr * mi;
+  } else {                  // adam with bias correction
+    T mi = *mi_io * b1;
+    mi += (T(1) - b1) * gi;
+    T vi = *vi_io * b2;
+    vi += (T(1) - b2) * gi * gi;
+    *mi_io = mi;
+    *vi_io = vi;
+    const T mh = mi / bc1, vh = vi / bc2;
+    pi -= lr * mh / (sqrt(vh) + eps);
+  }
+  return pi;
+}
+
+template <typename T>
 __global__ void optim_kernel(T* __restrict__ p, const T* __restrict__ g, T* __restrict__ m,
                              T* __restrict__ v, int64_t n, int kind, T lr, T b1, T b2, T eps,
                              T bc1, T bc2, T mom, __nv_bfloat16* __restrict__ shadow,
@@ -726,28 +749,63 @@ __global__ void optim_kernel(T* __restrict__ p, const T* __restrict__ g, T* __re
   int bad = 0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const T gi = g[i];
-    T pi = p[i];
-    if (kind == 0) {          // sgd
-      pi -= lr * gi;
-    } else if (kind == 1) {   // momentum: m = mu*m + g ; p -= lr*m
-      T mi = m[i] * mom;
-      mi += gi;
-      m[i] = mi;
-      pi -= lr * mi;
-    } else {                  // adam with bias correction
-      T mi = m[i] * b1;
-      mi += (T(1) - b1) * gi;
-      T vi = v[i] * b2;
-      vi += (T(1) - b2) * gi * gi;
-      m[i] = mi;
-      v[i] = vi;
-      const T mh = mi / bc1, vh = vi / bc2;
-      pi -= lr * mh / (sqrt(vh) + eps);
-    }
+    T mi = kind >= 1 ? m[i] : T(0), vi = kind == 2 ? v[i] : T(0);
+    const T pi = optim_elem<T>(p[i], g[i], &mi, &vi, kind, lr, b1, b2, eps, bc1, bc2, mom);
+    if (kind >= 1) m[i] = mi;
+    if (kind == 2) v[i] = vi;
     p[i] = pi;
     bad |= !isfinite(pi);
     if (shadow && i < n_shadow) shadow[i] = __float2bfloat16_rn(static_cast<float>(pi));
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(nonfinite, 1);
+}
+
+// fp32 master weights, 16-byte aligned: four parameters per thread iteration
+// (float4 loads / stores, the same per-element arithmetic as optim_kernel);
+// the n % 4 tail is the scalar loop's.
+__global__ void optim_f32x4_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                                   float* __restrict__ v, int64_t n, int kind, float lr, float b1, float b2,
+                                   float eps, float bc1, float bc2, float mom, __nv_bfloat16* __restrict__ shadow,
+                                   int64_t n_shadow, int* __restrict__ nonfinite) {
+  int bad = 0;
+  const int64_t n4 = n >> 2;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
+    float4 pv = reinterpret_cast<const float4*>(p)[q];
+    const float4 gv = __ldcs(reinterpret_cast<const float4*>(g) + q);
+    float4 mv = kind >= 1 ? reinterpret_cast<const float4*>(m)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 vv = kind == 2 ? reinterpret_cast<const float4*>(v)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    pv.x = optim_elem<float>(pv.x, gv.x, &mv.x, &vv.x, kind, lr, b1, b2, eps, bc1, bc2, mom);
+    pv.y = optim_elem<float>(pv.y, gv.y, &mv.y, &vv.y, kind, lr, b1, b2, eps, bc1, bc2, mom);
+    pv.z = optim_elem<float>(pv.z, gv.z, &mv.z, &vv.z, kind, lr, b1, b2, eps, bc1, bc2, mom);
+    pv.w = optim_elem<float>(pv.w, gv.w, &mv.w, &vv.w, kind, lr, b1, b2, eps, bc1, bc2, mom);
+    if (kind >= 1) reinterpret_cast<float4*>(m)[q] = mv;
+    if (kind == 2) reinterpret_cast<float4*>(v)[q] = vv;
+    reinterpret_cast<float4*>(p)[q] = pv;
+    bad |= !(isfinite(pv.x) && isfinite(pv.y) && isfinite(pv.z) && isfinite(pv.w));
+    const int64_t i = q << 2;
+    if (shadow) {
+      if (i + 3 < n_shadow) {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(pv.x, pv.y), hi = __floats2bfloat162_rn(pv.z, pv.w);
+        uint2 u;
+        u.x = *reinterpret_cast<const uint32_t*>(&lo);
+        u.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(shadow + i) = u;
+      } else {
+        const float e[4] = {pv.x, pv.y, pv.z, pv.w};
+        for (int t = 0; t < 4; ++t)
+          if (i + t < n_shadow) shadow[i + t] = __float2bfloat16_rn(e[t]);
+      }
+    }
+  }
+  for (int64_t i = (n4 << 2) + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float mi = kind >= 1 ? m[i] : 0.f, vi = kind == 2 ? v[i] : 0.f;
+    const float pi = optim_elem<float>(p[i], g[i], &mi, &vi, kind, lr, b1, b2, eps, bc1, bc2, mom);
+    if (kind >= 1) m[i] = mi;
+    if (kind == 2) v[i] = vi;
+    p[i] = pi;
+    bad |= !isfinite(pi);
+    if (shadow && i < n_shadow) shadow[i] = __float2bfloat16_rn(pi);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(nonfinite, 1);
 }
@@ -959,6 +1017,14 @@ int moep_optim_step(const moep_optim_args* a, void* stream) {
         static_cast<double*>(a->params), static_cast<const double*>(a->grads), static_cast<double*>(a->m),
         static_cast<double*>(a->v), a->n, a->kind, a->lr, a->beta1, a->beta2, a->eps, bc1, bc2, a->momentum,
         static_cast<__nv_bfloat16*>(a->shadow_bf16), a->n_shadow, a->nonfinite);
+  else if (a->dtype == MOEP_F32 && ((reinterpret_cast<uintptr_t>(a->params) | reinterpret_cast<uintptr_t>(a->grads) |
+                                       reinterpret_cast<uintptr_t>(a->m) | reinterpret_cast<uintptr_t>(a->v) |
+                                       reinterpret_cast<uintptr_t>(a->shadow_bf16)) & 15) == 0)
+    optim_f32x4_kernel<<<grid, 256, 0, st>>>(
+        static_cast<float*>(a->params), static_cast<const float*>(a->grads), static_cast<float*>(a->m),
+        static_cast<float*>(a->v), a->n, a->kind, static_cast<float>(a->lr), static_cast<float>(a->beta1),
+        static_cast<float>(a->beta2), static_cast<float>(a->eps), static_cast<float>(bc1), static_cast<float>(bc2),
+        static_cast<float>(a->momentum), static_cast<__nv_bfloat16*>(a->shadow_bf16), a->n_shadow, a->nonfinite);
   else if (a->dtype == MOEP_F32)
     optim_kernel<float><<<grid, 256, 0, st>>>(
         static_cast<float*>(a->params), static_cast<const float*>(a->grads), static_cast<float*>(a->m),
