@@ -504,12 +504,21 @@ int moep_num_sms(void) {
 
 const char* moep_version(void) { return "moep_b200 0.1 sm_100a"; }
 
+int moep_k7b_eval(const void* z, int32_t dtype, int64_t n, int32_t E, const int32_t* truth, int32_t k,
+                  int32_t n_m, const int32_t* m_list, int32_t* partials, int32_t ncnt, void* stream);
+int moep_k7b_topk(const void* z, int32_t dtype, int64_t n, int32_t E, int32_t m, int32_t* ids, void* stream);
+
 int moep_eval_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, const int32_t* truth,
                      int32_t k, int32_t n_m, const int32_t* m_list, int32_t* partials, void* stream) {
   using namespace moep::k7;
   if (n <= 0 || E <= 0) return MOEP_ESHAPE;
   if (k < 1 || k > 16 || k > E || n_m < 1 || n_m > MOEP_MAX_BOUNDS) return MOEP_EARG;
   const int ncnt = moep_n_counters(n_m, E);
+  // one thread per token, packed-key networks (k7b_rows.cu): E in {16, 32, 64}
+  if (E == 16 || E == 32 || E == 64) {
+    const int rc = moep_k7b_eval(logits, dtype, n, E, truth, k, n_m, m_list, partials, ncnt, stream);
+    if (rc != MOEP_EUNSUPPORTED) return rc;
+  }
   const size_t smem = sizeof(int) * 2 * E * (NT / 32);
   if (smem > 200 * 1024) return MOEP_EUNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -571,6 +580,10 @@ int moep_topk_logits(const void* logits, int32_t dtype, int64_t n, int32_t E, in
   using namespace moep::k7;
   if (n <= 0 || E <= 0) return MOEP_ESHAPE;
   if (m < 1 || m > E) return MOEP_EARG;
+  if (E == 16 || E == 32 || E == 64) {
+    const int rc = moep_k7b_topk(logits, dtype, n, E, m, ids, stream);
+    if (rc != MOEP_EUNSUPPORTED) return rc;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = moep_num_sms() * 4;
   if (E <= 256 && m <= 16) {
