@@ -321,6 +321,113 @@ eval_rows_kernel(const T* __restrict__ z, int64_t n, const int* __restrict__ tru
   }
 }
 
+// K3 labels (losses.py BatchLabels: rank_of = 1 + stable descending rank,
+// topk_mask = rank < k, and the strict pairs among the top T = min(10, E) of
+// the ranking loss, losses.py:198-207): the full row sorted by one bitonic
+// network of E packed keys. Rows whose order the packed keys cannot certify
+// (two adjacent keys equal in their top 26 bits, or NaN inside the top T)
+// recompute ranks and pairs exactly from the staged values.
+constexpr int NTL = 256;
+
+template <typename T, int E>
+__global__ void __launch_bounds__(NTL)
+labels_rows_kernel(const T* __restrict__ sc, int64_t n, int k, int top_cut, int* __restrict__ rank_of,
+                   uint8_t* __restrict__ mask, int* __restrict__ pairs) {
+  using R = Row<T, E>;
+  static_assert(sizeof(T) >= sizeof(int), "rank staging reuses the value slots");
+  extern __shared__ __align__(16) unsigned char k7b_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* stg = reinterpret_cast<T*>(k7b_smem) + warp * 32 * R::S;
+  T* myrow = stg + lane * R::S;
+  int* myrank = reinterpret_cast<int*>(myrow);  // this row's ranks overwrite its own values
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NTL / 32) + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (NTL / 32);
+  for (int64_t r0 = gw * 32; r0 < n; r0 += nw * 32) {
+    stage_rows<T, E>(sc, r0, n, stg, lane);
+    __syncwarp();
+    const int64_t row = r0 + lane;
+    uint32_t key[E];
+#pragma unroll
+    for (int c = 0; c < E; c += R::V) {
+      T v[R::V];
+      *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(myrow + c);
+#pragma unroll
+      for (int u = 0; u < R::V; ++u) key[c + u] = (okey(v[u]) & ~63u) | static_cast<uint32_t>(63 - (c + u));
+    }
+    sort_desc<E>(key);
+    bool amb = false;
+#pragma unroll
+    for (int i = 1; i < E; ++i) amb |= ambiguous(key[i - 1], key[i]);
+    uint32_t tcut = key[0];
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (i == top_cut - 1) tcut = key[i];
+    amb |= (tcut & ~63u) == 0u;  // NaN inside the top T
+    int np = top_cut * (top_cut - 1) / 2;
+    uint64_t sel = 0;
+    if (row < n && amb) {
+      int rk[E];
+      for (int e = 0; e < E; ++e) rk[e] = exact_rank<T, E>(myrow, e);
+      np = 0;
+      for (int a = 0; a < E; ++a)
+        for (int b = 0; b < E; ++b)
+          np += (rk[a] < top_cut && rk[b] < top_cut && myrow[a] > myrow[b]) ? 1 : 0;
+      for (int e = 0; e < E; ++e) {
+        myrank[e] = rk[e] + 1;
+        if (rk[e] < k) sel |= 1ull << e;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int e = pk_index(key[i]);
+        myrank[e] = i + 1;
+        if (i < k) sel |= 1ull << e;
+      }
+    }
+    if (row < n) {
+      if (pairs) pairs[row] = np;
+#pragma unroll
+      for (int c = 0; c < E; c += 16) {  // 16 mask bytes per store: bit e -> byte e
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t b = static_cast<uint32_t>(sel >> (c + 4 * q)) & 0xfu;
+          w[q] = (b & 1u) | ((b & 2u) << 7) | ((b & 4u) << 14) | ((b & 8u) << 21);
+        }
+        *reinterpret_cast<uint4*>(mask + row * E + c) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    __syncwarp();
+    // coalesced copy of the warp's rank rows
+    const int64_t rows = n - r0 < 32 ? n - r0 : 32;
+    int* dst = rank_of + r0 * E;
+    for (int i = lane; i < rows * E; i += 32) dst[i] = reinterpret_cast<const int*>(stg + (i / E) * R::S)[i % E];
+    __syncwarp();
+  }
+}
+
+template <typename T, int E>
+int launch_labels(const T* sc, int64_t n, int k, int top_cut, int* rank_of, uint8_t* mask, int* pairs,
+                  cudaStream_t st) {
+  using R = Row<T, E>;
+  const size_t smem = sizeof(T) * (NTL / 32) * 32 * R::S;
+  auto kern = labels_rows_kernel<T, E>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+      return MOEP_ELAUNCH;
+    attr = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTL, smem) != cudaSuccess || per_sm < 1)
+    return MOEP_ELAUNCH;
+  const int64_t want = (n + NTL - 1) / NTL;
+  const int64_t cap = static_cast<int64_t>(per_sm) * moep_num_sms();
+  kern<<<static_cast<int>(want < cap ? want : cap), NTL, smem, st>>>(sc, n, k, top_cut, rank_of, mask, pairs);
+  return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
+}
+
 template <typename T, int E, int G>
 int launch_topk(const T* z, int64_t n, int m, int* ids, cudaStream_t st) {
   using R = Row<T, E>;
@@ -401,6 +508,25 @@ extern "C" int moep_k7b_eval(const void* z, int32_t dtype, int64_t n, int32_t E,
     if (E == 16) return launch_eval<double, 16, 16>(p, n, truth, k, n_m, m_list, partials, ncnt, st);
     if (E == 32) return launch_eval<double, 32, 16>(p, n, truth, k, n_m, m_list, partials, ncnt, st);
     if (E == 64) return launch_eval<double, 64, 16>(p, n, truth, k, n_m, m_list, partials, ncnt, st);
+  }
+  return MOEP_EUNSUPPORTED;
+}
+
+extern "C" int moep_k7b_labels(const void* sc, int32_t dtype, int64_t n, int32_t E, int32_t k, int32_t top_cut,
+                               int32_t* rank_of, uint8_t* mask, int32_t* pairs, void* stream) {
+  using namespace moep::k7b;
+  if ((reinterpret_cast<uintptr_t>(sc) | reinterpret_cast<uintptr_t>(mask)) & 15) return MOEP_EUNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == MOEP_F32) {
+    const float* p = static_cast<const float*>(sc);
+    if (E == 16) return launch_labels<float, 16>(p, n, k, top_cut, rank_of, mask, pairs, st);
+    if (E == 32) return launch_labels<float, 32>(p, n, k, top_cut, rank_of, mask, pairs, st);
+    if (E == 64) return launch_labels<float, 64>(p, n, k, top_cut, rank_of, mask, pairs, st);
+  } else if (dtype == MOEP_F64) {
+    const double* p = static_cast<const double*>(sc);
+    if (E == 16) return launch_labels<double, 16>(p, n, k, top_cut, rank_of, mask, pairs, st);
+    if (E == 32) return launch_labels<double, 32>(p, n, k, top_cut, rank_of, mask, pairs, st);
+    if (E == 64) return launch_labels<double, 64>(p, n, k, top_cut, rank_of, mask, pairs, st);
   }
   return MOEP_EUNSUPPORTED;
 }

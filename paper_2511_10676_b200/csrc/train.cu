@@ -841,6 +841,9 @@ static int launch_loss(const moep_loss_args* a, const LossParams& p, cudaStream_
 
 extern "C" {
 
+int moep_k7b_labels(const void* sc, int32_t dtype, int64_t n, int32_t E, int32_t k, int32_t top_cut,
+                    int32_t* rank_of, uint8_t* mask, int32_t* pairs, void* stream);
+
 int moep_labels(const void* scores, int32_t dtype, int64_t n, int32_t E, int32_t k, int32_t* rank_of,
                 uint8_t* topk_mask, int32_t* pair_count, void* stream) {
   if (n <= 0 || E <= 0) return MOEP_ESHAPE;
@@ -848,6 +851,10 @@ int moep_labels(const void* scores, int32_t dtype, int64_t n, int32_t E, int32_t
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = moep_num_sms() * 8;  // 8 CTAs of 256 per SM: hide the per-token shuffle chains
   const int top_cut = E < 10 ? E : 10;  // TOP_TIER_SIZE (losses.py:27)
+  if (E == 16 || E == 32 || E == 64) {  // one thread per token, sorting network (k7b_rows.cu)
+    const int rc = moep_k7b_labels(scores, dtype, n, E, k, top_cut, rank_of, topk_mask, pair_count, stream);
+    if (rc != MOEP_EUNSUPPORTED) return rc;
+  }
   if (E <= 256) {
 #define MOEP_K3(T, LPR, EPL)                                                                                \
   labels_reg_kernel<T, LPR, EPL><<<grid, NT, 0, st>>>(static_cast<const T*>(scores), n, E, k, top_cut, rank_of, \

@@ -79,3 +79,28 @@ def test_k7b_eval_vs_oracle(O, dtype, e, k, ms):
         assert got.recall[m] == ref["recall_count"][m], m
     assert np.array_equal(got.per_expert_hits, ref["per_expert_hits"])
     assert np.array_equal(got.per_expert_truth, ref["per_expert_truth"])
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("e,k", [(16, 2), (32, 4), (64, 6)])
+def test_k3_labels_rows_vs_oracle(O, dtype, e, k):
+    """K3 (moep_labels) one thread per token: rank_of, topk_mask and the strict
+    pairs among the top min(10, E) (losses.py:198-207) equal the oracle's on
+    adversarial rows (exact ties, near-ties, signed zeros, infinities)."""
+    from paper_2511_10676_b200._lib import check, lib, ptr, dtype_code
+    n = 3001
+    z = _rows(n, e, 7 * e + k, dtype)
+    z = np.where(np.isnan(z), 0.25, z).astype(dtype)
+    s = torch.from_numpy(z).cuda()
+    rank = torch.empty((n, e), dtype=torch.int32, device="cuda")
+    mask = torch.empty((n, e), dtype=torch.uint8, device="cuda")
+    pairs = torch.empty(n, dtype=torch.int32, device="cuda")
+    check(lib().moep_labels(ptr(s), dtype_code(s), n, e, k, ptr(rank), ptr(mask), ptr(pairs), None), "moep_labels")
+    ref = O.batch_labels(z.astype(np.float64), k)
+    assert np.array_equal(rank.cpu().numpy(), ref["rank_of"])
+    assert np.array_equal(mask.cpu().numpy().astype(bool), ref["topk_mask"])
+    top_cut = min(10, e)
+    zz = z.astype(np.float64)
+    want = np.array([int(((zz[i][ref["rank_of"][i] <= top_cut])[:, None] >
+                          (zz[i][ref["rank_of"][i] <= top_cut])[None, :]).sum()) for i in range(n)])
+    assert np.array_equal(pairs.cpu().numpy(), want)
