@@ -120,7 +120,7 @@ def make_layers(dev, n_layers, tokens, seed_base, kind=WORKLOAD):
 
 def _k1_traffic(tokens):
     """DRAM bytes per K1 launch from the committed ncu capture (None if absent)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_k1_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_k1_traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)
@@ -288,7 +288,7 @@ def main():
                          "k1_ms_standalone": k1_ms_standalone, "pipeline_ms_per_layer": pipe_ms,
                          "traffic": _k1_traffic(args.tokens),
                          "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch, "
-                                           "ncu --set full (profiles/r01_k1_traffic.json), scaled to tokens"},
+                                           "ncu --set full (profiles/r02_k1_traffic.json), scaled to tokens"},
             # per layer: K1 pair kernel; fix-up: GEMM, split-hidden kernel + its finish (exit
             # at once unless <= 256 rows are flagged), GEMM finish, overflow K2 (exits unless
             # the capacity overflows); counter reduce
