@@ -53,7 +53,7 @@ for _ in range(3): run()
 torch.cuda.synchronize()
 run(); torch.cuda.synchronize()
 buf = np.zeros((16, 64), dtype=np.int64)
-fn = L.moep_k1v4_trace if os.environ.get("MOEP_K1_VARIANT") == "4" else L.moep_k1_trace
+fn = L.moep_k1_trace if os.environ.get("MOEP_K1_TRACE") == "v2" else L.moep_k1v4_trace  # 1 M tokens: v4 runs
 fn.argtypes = [C.c_void_p]
 fn(buf.ctypes.data)
 print(json.dumps(buf.tolist()))

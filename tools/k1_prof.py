@@ -42,11 +42,11 @@ if __name__ == "__main__":
     import bench
     from paper_2511_10676_b200 import _lib
     L = _lib.lib()
-    V3 = os.environ.get("MOEP_K1_VARIANT", "2") == "3"
-    prof = L.moep_k1v3_prof if V3 else L.moep_k1_prof
+    prof = L.moep_k1_prof  # role counters exist in the v2 pair kernel only
     prof.argtypes = [C.c_void_p, C.c_int]
     layers = bench.make_layers(torch.device("cuda"), 1, bench.TOKENS, 0)
     _, dp, x, t = layers[0]
+    dp.k1_kernel = _lib.MOEP_K1_PAIR_V2
     part = torch.empty((148, 136), dtype=torch.int32, device="cuda")
     run = lambda: dp._k1(x, m_sel=0, bounds=(1, 6, 10), truth=t, k=6, m_values=[6, 10, 64], partials=part)
     for _ in range(3):
