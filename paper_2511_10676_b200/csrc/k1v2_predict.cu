@@ -429,6 +429,12 @@ predict_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_const
           float* zrow = k1c::zstage_row<EP>(smem + C::OFF_A2, row_in_tile, lane, zswz);
           k1c::row_epilogue<EP>(p, z, sumsq, row_g, row_g < p.n_tokens, lane, hist, rc, zrow, zswz);
           K1_TR(15, gc - 1, lane == 0 && q == 0);
+          // A warp's A2 rows for the next chunk (swizzled 128-byte rows in each of
+          // the four atoms) overlap OTHER warps' staging rows: no warp of WG0 may
+          // leave the token epilogue (and write A2) while another still reads
+          // its staging row (the selection and the truth-window checks run for
+          // data-dependent times per warp)
+          asm volatile("bar.sync 4, 128;" ::: "memory");
         }
       }
     }

@@ -491,3 +491,32 @@ def test_v5_cluster_kernel_evaluate(pb, O, n, e, arch):
     assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
     assert np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
     assert np.array_equal(c.per_expert_truth, oc["per_expert_truth"])
+
+
+@pytest.mark.parametrize("e,k", [(128, 8), (16, 2)])
+def test_v2_token_epilogue_staging_race(pb, O, e, k):
+    """K1 v2 stages each token's logits in the A2 shared-memory region, whose
+    per-warp A2 rows overlap OTHER warps' staging rows: a warp that finished
+    its (data-dependent) selection must not write the next chunk's A2 while
+    another still reads its staging row (found as a rare counter mismatch in a
+    full-suite run; fixed with a warpgroup barrier). Repeated evaluations with
+    truth-heavy windows must all equal the oracle."""
+    rng = np.random.default_rng(4242 + e)
+    n, d, h = 20480, 1024, 1024
+    m = bf16_model(pb, O, "arch2", d, h, e, seed=8)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref = O.predict_logits(oracle_params(m), x)
+    truth = O.top_k_batch(zref + 0.02 * rng.standard_normal(zref.shape), k)
+    ms = O.default_m_list(k, e)
+    oc = O.eval_counters(zref, truth, e, ms)
+    dev = m.to_device()
+    dev.k1_kernel = 2
+    dev.decode_max_tokens = 0
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    tt = torch.from_numpy(truth)
+    for _ in range(6):
+        cnt, _, _ = dev.evaluate(xt, tt, k, ms)
+        c = pb.EvalCounters.from_array(cnt.cpu().numpy(), k, e, sorted(set(ms) | {k}))
+        assert c.n == oc["n"] and c.top1 == oc["top1_count"]
+        assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
+        assert np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
