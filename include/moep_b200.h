@@ -88,6 +88,11 @@ typedef struct {
                                  ConfigurationError (predictor.py:188-189), without a separate
                                  isfinite pass over x in the common case. */
   int32_t kernel;             /* MOEP_K1_AUTO (0) or a forced kernel (tests / measurements) */
+  float* probs;               /* [N, E] fp32 softmax of the logits (core.softmax, core.py:19-24:
+                                 exp(z - max) / sum, fused into the token epilogue), or NULL.
+                                 From K1's fp32 logits for every row (flagged or not): each
+                                 logit is within delta/2 of exact, so |p - p_ref| <= p_ref *
+                                 (exp(delta) - 1) + 2^-22. */
 } moep_predict_args;
 
 enum { MOEP_K1_AUTO = 0, MOEP_K1_ONE_SM = 1, MOEP_K1_PAIR_V2 = 2, MOEP_K1_PAIR_V4 = 4, MOEP_K1_QUAD_V5 = 5 };

@@ -33,7 +33,7 @@ class PredictArgs(C.Structure):
         ("tau_abs", f32), ("tau_rel", f32), ("w2_norm", f32),
         ("ids", vp), ("logits", vp), ("flags", vp), ("flag_list", vp), ("flag_count", vp),
         ("truth", vp), ("k", i32), ("n_m", i32), ("m_list", i32 * MAX_BOUNDS), ("partials", vp),
-        ("a_out", vp), ("split_scratch", vp), ("split_scratch_floats", i64), ("status", vp), ("kernel", i32),
+        ("a_out", vp), ("split_scratch", vp), ("split_scratch_floats", i64), ("status", vp), ("kernel", i32), ("probs", vp),
     ]
 
 

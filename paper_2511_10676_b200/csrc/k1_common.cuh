@@ -30,6 +30,7 @@ struct Params {
   int n_counters;
   float* a_out;
   int* status;  // bit 0: some token's fp32 logits were non-finite (host checks the input)
+  float* probs;  // [N, E] fused softmax of the fp32 logits, or nullptr
   // hidden split (pair kernel, small N): `split` chunk groups per 256-token tile;
   // partial z [split][zpad][EP] and partial ||h||^2 [split][zpad] in zpart
   int split;
@@ -99,6 +100,23 @@ __device__ __forceinline__ bool test(uint64_t* bar, uint32_t parity) {
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return done != 0;
+}
+
+// Max-subtracted softmax of one token's logits (core.softmax, core.py:19-24:
+// e = exp(z - max(z)); e / e.sum()) into out[0, E), fp32 with expf.
+template <int EP, class ZGet>
+__device__ __forceinline__ void softmax_row(ZGet zv, int E, float* out) {
+  float mx = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < EP; ++e)
+    if (e < E) mx = fmaxf(mx, zv(e));
+  float s = 0.f;
+#pragma unroll
+  for (int e = 0; e < EP; ++e)
+    if (e < E) s += expf(zv(e) - mx);
+#pragma unroll
+  for (int e = 0; e < EP; ++e)
+    if (e < E) out[e] = expf(zv(e) - mx) / s;
 }
 
 // z[EP]: this token's raw GEMM2 accumulator (no b2). Every lane of the warp
@@ -209,6 +227,7 @@ __device__ __forceinline__ void row_epilogue_core(const Params& p, ZGet zv, bool
       for (int e = 0; e < EP; ++e)
         if (e < p.E) lrow[e] = zv(e);
     }
+    if (p.probs) softmax_row<EP>(zv, p.E, p.probs + row * p.E);
     if (p.ids && !flagged) {
       int* orow = p.ids + row * p.m_sel;
       if (p.m_sel >= p.E) {

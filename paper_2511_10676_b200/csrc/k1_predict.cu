@@ -78,6 +78,7 @@ struct Params {
   int n_counters;
   float* a_out;
   int* status;
+  float* probs;  // [N, E] fused softmax of the fp32 logits, or nullptr
 };
 
 // ------------------------------------------------------------------ kernel
@@ -396,6 +397,19 @@ predict_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
             for (int e = 0; e < EP; ++e)
               if (e < p.E) lrow[e] = z[e];
           }
+          if (p.probs) {  // fused softmax (core.py:19-24): exp(z - max) / sum
+            float mx = -INFINITY, sum = 0.f;
+#pragma unroll
+            for (int e = 0; e < EP; ++e)
+              if (e < p.E) mx = fmaxf(mx, z[e]);
+#pragma unroll
+            for (int e = 0; e < EP; ++e)
+              if (e < p.E) sum += expf(z[e] - mx);
+            float* prow = p.probs + row * p.E;
+#pragma unroll
+            for (int e = 0; e < EP; ++e)
+              if (e < p.E) prow[e] = expf(z[e] - mx) / sum;
+          }
           if (p.ids && !flagged) {
             int* orow = p.ids + row * p.m_sel;
             if (p.m_sel >= p.E) {
@@ -528,7 +542,7 @@ int launch_k1(const moep_predict_args* a, cudaStream_t st, const CUtensorMap& tx
   p.m_sel = a->m_sel; p.n_bounds = a->n_bounds;
   for (int i = 0; i < MOEP_MAX_BOUNDS; ++i) { p.bounds[i] = a->bounds[i]; p.m_list[i] = a->m_list[i]; }
   p.tau_abs = a->tau_abs; p.tau_rel = a->tau_rel; p.w2_norm = a->w2_norm;
-  p.ids = a->ids; p.logits = a->logits; p.flags = a->flags;
+  p.ids = a->ids; p.logits = a->logits; p.flags = a->flags; p.probs = a->probs;
   p.flag_list = a->flag_list; p.flag_count = a->flag_count;
   p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;
   p.status = a->status;

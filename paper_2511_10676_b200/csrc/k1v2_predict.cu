@@ -564,6 +564,25 @@ __global__ void __launch_bounds__(256) split_finish_kernel(const Params p) {
         if (e < E) p.logits[row * E + e] = zv[q];
       }
     }
+    if (p.probs) {  // fused softmax (core.py:19-24) across the warp's lanes
+      float mx = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < PL; ++q)
+        if (q * 32 + lane < E) mx = fmaxf(mx, zv[q]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float sum = 0.f;
+#pragma unroll
+      for (int q = 0; q < PL; ++q)
+        if (q * 32 + lane < E) sum += expf(zv[q] - mx);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const int e = q * 32 + lane;
+        if (e < E) p.probs[row * E + e] = expf(zv[q] - mx) / sum;
+      }
+    }
     if (p.ids && !flagged) {
       int* orow = p.ids + row * p.m_sel;
       if (p.m_sel >= E) {
@@ -743,7 +762,7 @@ int launch_v2(const moep_predict_args* a, cudaStream_t st) {
   p.m_sel = a->m_sel; p.n_bounds = a->n_bounds;
   for (int i = 0; i < MOEP_MAX_BOUNDS; ++i) { p.bounds[i] = a->bounds[i]; p.m_list[i] = a->m_list[i]; }
   p.tau_abs = a->tau_abs; p.tau_rel = a->tau_rel; p.w2_norm = a->w2_norm;
-  p.ids = a->ids; p.logits = a->logits; p.flags = a->flags;
+  p.ids = a->ids; p.logits = a->logits; p.flags = a->flags; p.probs = a->probs;
   p.flag_list = a->flag_list; p.flag_count = a->flag_count;
   p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;
   p.status = a->status;

@@ -539,7 +539,7 @@ int launch_v5(const moep_predict_args* a, cudaStream_t st) {
   for (int i = 0; i < MOEP_MAX_BOUNDS; ++i) { p.bounds[i] = a->bounds[i]; p.m_list[i] = a->m_list[i]; }
   p.tau_abs = a->tau_abs; p.tau_rel = a->tau_rel; p.w2_norm = a->w2_norm;
   p.status = a->status;
-  p.ids = a->ids; p.logits = a->logits; p.flags = a->flags;
+  p.ids = a->ids; p.logits = a->logits; p.flags = a->flags; p.probs = a->probs;
   p.flag_list = a->flag_list; p.flag_count = a->flag_count;
   p.truth = a->truth; p.k = a->k; p.n_m = a->n_m; p.partials = a->partials; p.a_out = a->a_out;
   p.n_counters = moep_n_counters(a->n_m, a->n_experts);

@@ -273,7 +273,7 @@ class DevicePredictor:
         return a
 
     def _k1(self, xb, m_sel=0, bounds=(), ids=None, logits=None, truth=None, k=0, m_values=(),
-            partials=None, status=None, kernel=0):
+            partials=None, status=None, kernel=0, probs=None):
         n = xb.shape[0]
         flags = torch.empty(n, dtype=torch.uint8, device=self.device)
         flag_list = torch.empty(n, dtype=torch.int32, device=self.device)
@@ -299,6 +299,7 @@ class DevicePredictor:
         scratch = torch.empty(need, dtype=torch.float32, device=self.device) if need else None
         a.split_scratch, a.split_scratch_floats = ptr(scratch), need
         a.status, a.kernel = ptr(status), int(kernel or self.k1_kernel)
+        a.probs = ptr(probs)
         check(lib().moep_predict_bf16(a, _stream(self.device)), "moep_predict_bf16")
         return flags, flag_list, flag_count
 
@@ -355,6 +356,24 @@ class DevicePredictor:
         else:
             out64 = self.logits_fp64_all(x)
         return (out64, flags) if return_flags else out64
+
+    def probs(self, x: torch.Tensor, validate=True) -> torch.Tensor:
+        """Expert probabilities [N, E] fp32: the softmax (core.softmax,
+        core.py:19-24) fused into K1's token epilogue (north_star (1): ...
+        -> softmax -> top-k). Computed from K1's fp32 logits for every row:
+        each logit is within delta/2 of its exact value, so
+        |p - p_ref| <= p_ref (exp(delta) - 1) + 2^-22 (test_gpu_parity.py).
+        Inputs the tensor-core path cannot take: softmax of the exact fp64
+        logits."""
+        x, xb, exact = self.prepare(x)
+        if not self.k1_usable(exact):
+            return torch.softmax(self.logits_fp64_all(x), dim=1).float()
+        pr = torch.empty((x.shape[0], self.E), dtype=torch.float32, device=self.device)
+        status = self.new_status()
+        self._k1(xb, probs=pr, status=status)
+        if validate:
+            self.check_status(status, x)
+        return pr
 
     def fp64_rows(self, xb: torch.Tensor, out64: torch.Tensor, row0: int = 0, row1: int | None = None,
                   chunk: int = 1 << 16) -> torch.Tensor:

@@ -520,3 +520,27 @@ def test_v2_token_epilogue_staging_race(pb, O, e, k):
         assert c.n == oc["n"] and c.top1 == oc["top1_count"]
         assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
         assert np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
+
+
+@pytest.mark.parametrize("arch,d,h,e,n", [("arch2", 2048, 2048, 64, 40000), ("arch2", 2048, 2048, 128, 20480),
+                                          ("arch2", 1024, 1024, 16, 300), ("arch1", 1024, 1024, 32, 5000),
+                                          ("arch2", 256, 384, 32, 2000)])
+def test_fused_softmax_probs(pb, O, arch, d, h, e, n):
+    """north_star (1)'s softmax stage: K1's fused softmax of its fp32 logits
+    (core.softmax, core.py:19-24) against softmax of the exact fp64 logits.
+    Each logit is within delta/2 of exact (the margin contract), so
+    |p - p_ref| <= p_ref (exp(delta) - 1 + 1e-5) + 2^-22 per row, where the
+    1e-5 covers the fp32 exp / sum / divide; rows sum to 1 within 1e-5.
+    Covers v4, v2 (one wave), the hidden split, arch1 and the 1-SM kernel."""
+    rng = np.random.default_rng(n + e)
+    m = bf16_model(pb, O, arch, d, h, e, seed=21, rng=rng)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref, cache = O.forward_eval(oracle_params(m), x)
+    dev = m.to_device()
+    p = dev.probs(torch.from_numpy(x).to("cuda", torch.bfloat16)).double().cpu().numpy()
+    pref = O.softmax(zref, axis=1)
+    hn = np.linalg.norm(cache["h"], axis=1)
+    delta = dev.tau_abs + dev.tau_bias + dev.tau_rel * (1.5 if e > 64 else 1.0) * hn * dev.w2_norm
+    bound = pref * (np.expm1(delta)[:, None] + 1e-5) + 2.0 ** -22
+    assert (np.abs(p - pref) <= bound).all(), np.abs(p - pref).max()
+    assert np.allclose(p.sum(axis=1), 1.0, rtol=0, atol=1e-5)
