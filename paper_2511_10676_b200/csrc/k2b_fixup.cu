@@ -25,6 +25,9 @@ namespace moep {
 namespace k2b {
 
 constexpr int TM = 64, TN = 128, KS = 16;
+#ifndef MOEP_FIX_TM
+#define MOEP_FIX_TM 64  // fix_gemm rows per CTA (32: the 4-warp tile, measured slower)
+#endif
 #ifndef MOEP_DEC_ROWS_MAX
 #define MOEP_DEC_ROWS_MAX 512
 #endif
@@ -79,9 +82,17 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 // DMMA fragment reads); the epilogue reuses it for hs[TM][TN+1].
 constexpr int AP = TM + 4, BP = TN + 4;
 
-template <int XT, int WT>
-__global__ void __launch_bounds__(NT, 2)
+// TM_ rows x TN hidden per CTA with NT_ threads (8 or 4 warps of 32 x 32):
+// 64 x 128 / 256 threads (2 CTAs per SM, the default) or 32 x 128 / 128
+// threads (4 per SM). The half-size tile was meant to cut the wave
+// quantisation at ~1,500 flagged rows (the 64-row grid is 1.35 waves), but
+// it measured slower: 0.65-0.69 ms vs 0.62 ms per 1 M-token layer (ncu launch
+// times, tools/prof_pipeline.py) -- twice the W1 tile traffic per row.
+template <int XT, int WT, int TM_ = TM, int NT_ = NT>
+__global__ void __launch_bounds__(NT_, 512 / NT_)
 fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
+  constexpr int TM = TM_, NT = NT_, AP = TM + 4;
+  static_assert(TM * TN / (NT / 32) == 32 * 32, "one 32 x 32 tile per warp");
   extern __shared__ double sm[];
   const int64_t count = a.rows ? static_cast<int64_t>(*a.row_count) : a.n_tokens;
   const int64_t nrows = count < cap ? count : cap;
@@ -106,20 +117,22 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
   // row n = tid % 128, k-half tid / 128) reads 8 consecutive k (one 16-byte bf16
   // load). Global loads of tile kt+1 are issued into registers before the
   // compute of tile kt and stored (converted to fp64) after it.
-  const int ar = tid & (TM - 1), akq = tid / TM;   // A: row, k-quarter
-  const int bn = tid & (TN - 1), bkh = tid / TN;   // B: hidden row, k-half
+  const int ar = tid & (TM - 1), akq = tid / TM;   // A: row, k-quarter (NT / TM = 4 quarters)
+  static_assert(NT / TM == 4, "A loader: 4 consecutive k per thread");
+  constexpr int BKH = NT / TN;                      // B k-groups covered per pass (2 or 1)
+  constexpr int BPASS = 2 / BKH;                    // passes of 8 k per thread
+  const int bn = tid & (TN - 1), bkh = tid / TN;   // B: hidden row, k-group
   const int64_t arow = rowid[ar];
   const int bj = h0 + bn;
   const bool vec = (d % 8) == 0;
-  uint32_t ua[2], ub[4];
-  double ra[(XT == MOEP_BF16) ? 1 : 4], rb[(WT == MOEP_BF16) ? 1 : 8];
-  bool a_vec, b_vec;
-  int ka_s, kb_s;
+  uint32_t ua[2], ub[BPASS][4];
+  double ra[(XT == MOEP_BF16) ? 1 : 4], rb[BPASS][(WT == MOEP_BF16) ? 1 : 8];
+  bool a_vec, b_vec[BPASS];
+  int ka_s, kb_s[BPASS];
   auto fetch = [&](int k0) {
-    const int ka = k0 + akq * 4, kb = k0 + bkh * 8;
-    ka_s = ka; kb_s = kb;
+    const int ka = k0 + akq * 4;
+    ka_s = ka;
     a_vec = vec && arow >= 0 && ka < d;
-    b_vec = vec && bj < H && kb < d;
     if (a_vec) {
       if constexpr (XT == MOEP_BF16) {
         const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.x) + arow * d + ka));
@@ -130,16 +143,22 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
         ra[0] = p0.x; ra[1] = p0.y; ra[2] = p1.x; ra[3] = p1.y;
       }
     }
-    if (b_vec) {
-      if constexpr (WT == MOEP_BF16) {
-        const uint4 u = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.w1) +
-                                                            static_cast<int64_t>(bj) * d + kb));
-        ub[0] = u.x; ub[1] = u.y; ub[2] = u.z; ub[3] = u.w;
-      } else {
-        const double2* s2 = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(a.w1) +
-                                                             static_cast<int64_t>(bj) * d + kb);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) { const double2 v = __ldg(s2 + c); rb[2 * c] = v.x; rb[2 * c + 1] = v.y; }
+    for (int pb = 0; pb < BPASS; ++pb) {
+      const int kb = k0 + (bkh + pb * BKH) * 8;
+      kb_s[pb] = kb;
+      b_vec[pb] = vec && bj < H && kb < d;
+      if (b_vec[pb]) {
+        if constexpr (WT == MOEP_BF16) {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.w1) +
+                                                              static_cast<int64_t>(bj) * d + kb));
+          ub[pb][0] = u.x; ub[pb][1] = u.y; ub[pb][2] = u.z; ub[pb][3] = u.w;
+        } else {
+          const double2* s2 = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(a.w1) +
+                                                               static_cast<int64_t>(bj) * d + kb);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) { const double2 v = __ldg(s2 + c); rb[pb][2 * c] = v.x; rb[pb][2 * c + 1] = v.y; }
+        }
       }
     }
   };
@@ -156,21 +175,25 @@ fix_gemm(moep_fp64_args a, int64_t cap, double* __restrict__ part) {
       As[(buf * KS + akq * 4 + c) * AP + ar] = v;
     }
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      double v;
-      if (b_vec) {
-        if constexpr (WT == MOEP_BF16) v = bf16_to_f64((c & 1) ? (ub[c >> 1] >> 16) : (ub[c >> 1] & 0xffffu));
-        else v = rb[c];
-      } else {
-        v = (bj < H && kb_s + c < d) ? ld1<WT>(a.w1, static_cast<int64_t>(bj) * d + kb_s + c) : 0.0;
+    for (int pb = 0; pb < BPASS; ++pb) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double v;
+        if (b_vec[pb]) {
+          if constexpr (WT == MOEP_BF16) v = bf16_to_f64((c & 1) ? (ub[pb][c >> 1] >> 16) : (ub[pb][c >> 1] & 0xffffu));
+          else v = rb[pb][c];
+        } else {
+          v = (bj < H && kb_s[pb] + c < d) ? ld1<WT>(a.w1, static_cast<int64_t>(bj) * d + kb_s[pb] + c) : 0.0;
+        }
+        Bs[(buf * KS + (bkh + pb * BKH) * 8 + c) * BP + bn] = v;
       }
-      Bs[(buf * KS + bkh * 8 + c) * BP + bn] = v;
     }
   };
   // fp64 tensor-core MMA: warp (wm, wn) owns a 32 x 32 tile = 4 x 4 m8n8 tiles;
   // lane (g, q) holds A[m + g][k + q], B[k + q][n + g], C[m + g][n + 2q .. +1]
   const int warp = tid >> 5, lane = tid & 31;
-  const int wm = warp & 1, wn = warp >> 1;
+  constexpr int WM = TM / 32;
+  const int wm = warp % WM, wn = warp / WM;
   const int g = lane >> 2, q4 = lane & 3;
   double acc[4][4][2];
 #pragma unroll
@@ -909,16 +932,18 @@ extern "C" int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t
   if (a->m_sel < 0 || a->m_sel > a->n_experts) return MOEP_EARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int ntile_h = (a->hidden + TN - 1) / TN;
-  const size_t smem_main = sizeof(double) * 2 * KS * (AP + BP);
-  const size_t smem_epi = sizeof(double) * (TM * (TN + 1));
+  // rows per CTA (see fix_gemm)
+  constexpr int FTM = MOEP_FIX_TM, FNT = FTM * 4;
+  const size_t smem_main = sizeof(double) * 2 * KS * (FTM + 4 + BP);
+  const size_t smem_epi = sizeof(double) * (FTM * (TN + 1));
   const size_t smem = smem_main > smem_epi ? smem_main : smem_epi;
   if (smem > 200 * 1024) return MOEP_EUNSUPPORTED;
   const bool xb = a->x_dtype == MOEP_BF16, wb = a->w_dtype == MOEP_BF16;
-  dim3 grid(static_cast<unsigned>((cap + TM - 1) / TM), ntile_h);
+  dim3 grid(static_cast<unsigned>((cap + FTM - 1) / FTM), ntile_h);
   auto go = [&](auto kern) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
       return MOEP_ELAUNCH;
-    kern<<<grid, NT, smem, st>>>(*a, cap, scratch);
+    kern<<<grid, FNT, smem, st>>>(*a, cap, scratch);
     return cudaGetLastError() == cudaSuccess ? MOEP_OK : MOEP_ELAUNCH;
   };
   // min(count, capacity) <= DEC_ROWS_MAX (decided on the device): the
@@ -927,10 +952,10 @@ extern "C" int moep_fixup_fp64(const moep_fp64_args* a, double* scratch, int64_t
   const bool big = cap > DEC_ROWS_MAX;
   int rc = MOEP_OK;
   if (big) {
-    if (xb && wb) rc = go(fix_gemm<MOEP_BF16, MOEP_BF16>);
-    else if (xb) rc = go(fix_gemm<MOEP_BF16, MOEP_F64>);
-    else if (wb) rc = go(fix_gemm<MOEP_F64, MOEP_BF16>);
-    else rc = go(fix_gemm<MOEP_F64, MOEP_F64>);
+    if (xb && wb) rc = go(fix_gemm<MOEP_BF16, MOEP_BF16, FTM, FNT>);
+    else if (xb) rc = go(fix_gemm<MOEP_BF16, MOEP_F64, FTM, FNT>);
+    else if (wb) rc = go(fix_gemm<MOEP_F64, MOEP_BF16, FTM, FNT>);
+    else rc = go(fix_gemm<MOEP_F64, MOEP_F64, FTM, FNT>);
     if (rc != MOEP_OK) return rc;
   }
   rc = launch_dec(a, cap, scratch, st);
