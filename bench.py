@@ -582,8 +582,21 @@ def c3_arm(dev, batches=(1, 8, 32, 128, 256), n_layers=48):
                                              xo), K3)
         x0, i0 = hps[0].pre_attention(hid, prefetch=False)
         oracle_ok = bool(np.array_equal(x0.double().cpu().numpy(), xo) and np.array_equal(i0.cpu().numpy(), ido))
+        # the same pre-attention work as one CUDA graph replay (deploy.GraphedHook)
+        gh = hps[0].graph(B)
+        tg = []
+        for _ in range(20):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(main)
+            xg, ig = gh.pre_attention(hid, prefetch=False)
+            e1.record(main)
+            torch.cuda.synchronize()
+            tg.append(e0.elapsed_time(e1))
+        graph_ok = bool(torch.equal(xg, x0) and torch.equal(ig, i0))
         r = np.array(rows)
-        out["batches"].append({"batch": B, "predict_ms": float(r[:, 0].mean()), "attention_ms": float(r[:, 1].mean()),
+        out["batches"].append({"batch": B, "predict_ms": float(r[:, 0].mean()),
+                               "predict_graph_ms": float(np.median(tg)), "graph_equals_eager": graph_ok,
+                               "attention_ms": float(r[:, 1].mean()),
                                "load_ms": float(r[:, 2].mean()), "stall_ms": float(r[:, 3].mean()),
                                "experts_loaded": float(r[:, 4].mean()),
                                "load_gbs": float(r[:, 4].mean() * pf.QWEN3_EXPERT_BYTES / (r[:, 2].mean() / 1e3) / 1e9),

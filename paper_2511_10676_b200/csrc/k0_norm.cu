@@ -172,7 +172,10 @@ norm_fast_kernel(const uint16_t* __restrict__ x, int64_t n, const double* __rest
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
       const int idx = t * 32 + lane;
-      v[t] = (rs < n && idx / (D / 8) < rh) ? __ldcs(src + idx) : make_uint4(0, 0, 0, 0);
+      // a ragged tail's padding rows repeat the last row (a zero row would take
+      // the exact-conversion and level-2 paths: 4x the time of a decode-size call)
+      const int si = idx / (D / 8) < rh ? idx : static_cast<int>(rh - 1) * (D / 8) + idx % (D / 8);
+      v[t] = rs < n ? __ldcs(src + si) : make_uint4(0, 0, 0, 0);
     }
   };
   for (int64_t r0 = wg * RPW; r0 < n; r0 += nw * RPW) {
@@ -191,12 +194,10 @@ norm_fast_kernel(const uint16_t* __restrict__ x, int64_t n, const double* __rest
       for (int t = 0; t < 16; ++t) {
         const int idx = t * 32 + lane;
         uint4* dst = stage + (idx >> 4) * kStageU4 + (idx & 15);
-        if (idx / (D / 8) < rows_here) {
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-                       "l"(src + idx) : "memory");
-        } else {
-          *dst = make_uint4(0, 0, 0, 0);
-        }
+        // padding rows of a ragged tail repeat the last row (see fetch)
+        const int si = idx / (D / 8) < rows_here ? idx : static_cast<int>(rows_here - 1) * (D / 8) + idx % (D / 8);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                     "l"(src + si) : "memory");
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
     } else {

@@ -107,3 +107,32 @@ def test_hook_point_deployment(pf):
     hp2.pre_attention(bad)
     with pytest.raises(pb.ConfigurationError):
         hp2.check()
+
+
+def test_hook_point_cuda_graph(pf):
+    """The captured pre_attention (HookPointPredictor.graph) gives the eager
+    path's x_hat and ids on new inputs, replay after replay, and drives the
+    prefetch; its launch cost is one graph replay."""
+    import paper_2511_10676_b200 as pb
+    from paper_2511_10676_b200.deploy import HookPointPredictor
+    from oracle import oracle as O
+    rng = np.random.default_rng(11)
+    d, h, E, m, B = 1024, 1024, 64, 6, 3
+    model = pb.init_model("arch2", d, h, E, seed=4)
+    model.w1, model.w2 = O.round_bf16(model.w1), O.round_bf16(model.w2)
+    gamma = rng.uniform(0.5, 1.5, d)
+    store, cache = pf.ExpertStore(E, 4096), pf.ExpertCache(E, 4096, E)
+    hp = HookPointPredictor(model, m, "rmsnorm", gamma, prefetcher=pf.Prefetcher(store, cache), gather_ctas=8)
+    gh = hp.graph(B)
+    ref = HookPointPredictor(model, m, "rmsnorm", gamma)
+    for step in range(4):
+        hidden = torch.from_numpy(O.round_bf16(2.0 * rng.standard_normal((B, d)))).cuda().to(torch.bfloat16)
+        x_hat, ids = gh.pre_attention(hidden)
+        xr, ir = ref.pre_attention(hidden, prefetch=False)
+        assert torch.equal(x_hat, xr) and torch.equal(ids, ir), step
+        hp.pf.done.synchronize()
+        for e in set(ids.cpu().numpy().ravel().tolist()):
+            s = int(cache.slot_of[e].item())
+            assert s >= 0 and torch.equal(cache.slot(s).cpu(), store.blob(e)), e
+    with pytest.raises(pb.ConfigurationError):
+        gh.pre_attention(torch.zeros((B + 1, d), dtype=torch.bfloat16, device="cuda"))
