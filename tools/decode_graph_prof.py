@@ -24,3 +24,25 @@ for B in (1, 8):
         gh.pre_attention(hid, prefetch=False)
     torch.cuda.synchronize()
 print("ok")
+
+# timing without a profiler: eager vs graph replay, CUDA events, median of 50
+import statistics  # noqa: E402
+for B in (1, 8, 32):
+    hid = torch.randn((B, D), device="cuda").to(torch.bfloat16)
+    gh = hp.graph(B)
+    res = {}
+    for name, fn in (("eager", lambda: hp.pre_attention(hid, prefetch=False)),
+                     ("graph", lambda: gh.pre_attention(hid, prefetch=False))):
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(50):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        res[name] = round(statistics.median(ts), 1)
+    print("B", B, "us", res)
