@@ -22,68 +22,12 @@
 #include <cstdint>
 #include <climits>
 #include "common.cuh"
+#include "sortnet.cuh"
 
 namespace moep {
 namespace k7b {
 
-// monotone unsigned image of the value: larger value -> larger key; -0 == +0;
-// NaN -> 0 (below -inf)
-__device__ __forceinline__ uint32_t okey(float v) {
-  int b = __float_as_int(v);
-  if (b == static_cast<int>(0x80000000u)) b = 0;
-  const uint32_t u = static_cast<uint32_t>(b >= 0 ? (b | 0x80000000) : ~b);
-  return ((b & 0x7fffffff) > 0x7f800000) ? 0u : u;
-}
-__device__ __forceinline__ uint32_t okey(double v) {
-  long long b = __double_as_longlong(v);
-  if (b == static_cast<long long>(0x8000000000000000ull)) b = 0;
-  const unsigned long long u = static_cast<unsigned long long>(b >= 0 ? (b | static_cast<long long>(0x8000000000000000ull)) : ~b);
-  const bool nan = (b & 0x7fffffffffffffffll) > 0x7ff0000000000000ll;
-  return nan ? 0u : static_cast<uint32_t>(u >> 32);  // top 32 bits (the low 6 are replaced by the index)
-}
-// exact reference order between (a, ia) and (b, ib) on the full values
-template <typename T>
-__device__ __forceinline__ bool exact_before(T a, int ia, T b, int ib) {
-  const bool na = a != a, nb = b != b;
-  if (na || nb) return (!na && nb) || (na && nb && ia < ib);  // NaN last, ties by index
-  return a > b || (a == b && ia < ib);
-}
-
-template <int G>
-__device__ __forceinline__ void ce(uint32_t (&a)[G], int i, int j) {  // a[i] >= a[j] afterwards
-  const uint32_t x = a[i], y = a[j];
-  a[i] = max(x, y);
-  a[j] = min(x, y);
-}
-// descending bitonic sort of G keys
-template <int G>
-__device__ __forceinline__ void sort_desc(uint32_t (&a)[G]) {
-#pragma unroll
-  for (int size = 2; size <= G; size <<= 1)
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1)
-#pragma unroll
-      for (int i = 0; i < G; ++i) {
-        const int j = i ^ stride;
-        if (j > i) {
-          if ((i & size) == 0 || size == G) ce<G>(a, i, j);
-          else ce<G>(a, j, i);
-        }
-      }
-}
-// a <- top G of (a, b), both sorted descending
-template <int G>
-__device__ __forceinline__ void merge_top(uint32_t (&a)[G], const uint32_t (&b)[G]) {
-#pragma unroll
-  for (int i = 0; i < G; ++i) a[i] = max(a[i], b[G - 1 - i]);  // bitonic
-#pragma unroll
-  for (int stride = G >> 1; stride > 0; stride >>= 1)
-#pragma unroll
-    for (int i = 0; i < G; ++i) {
-      const int j = i ^ stride;
-      if (j > i) ce<G>(a, i, j);
-    }
-}
+using namespace moep::sortnet;
 
 // staged row stride (elements): 16-byte pad, conflict-free 16-byte per-lane reads
 template <typename T, int E>
@@ -134,10 +78,6 @@ __device__ __forceinline__ void top_keys(const T* myrow, uint32_t (&top)[G]) {
       merge_top<G>(top, grp);
     }
   }
-}
-__device__ __forceinline__ int pk_index(uint32_t p) { return 63 - static_cast<int>(p & 63u); }
-__device__ __forceinline__ bool ambiguous(uint32_t hi_side, uint32_t lo_side) {
-  return ((hi_side ^ lo_side) & ~63u) == 0;
 }
 
 // exact: number of experts before expert t in the reference order
