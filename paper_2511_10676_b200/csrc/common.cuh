@@ -52,6 +52,26 @@ __device__ __forceinline__ __nv_bfloat16 f64_to_bf16_rne(double x) {
   return __float2bfloat16_rn(static_cast<float>(r));                // exact (or inf on overflow)
 }
 
+// 16-byte chunk <-> register elements without taking a register array's
+// address (a reinterpret_cast of the array forces it into local memory)
+__device__ __forceinline__ void unpack16(const uint4& q, float* v) {
+  v[0] = __uint_as_float(q.x); v[1] = __uint_as_float(q.y); v[2] = __uint_as_float(q.z); v[3] = __uint_as_float(q.w);
+}
+__device__ __forceinline__ void unpack16(const uint4& q, double* v) {
+  v[0] = __hiloint2double(static_cast<int>(q.y), static_cast<int>(q.x));
+  v[1] = __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z));
+}
+__device__ __forceinline__ void unpack16(const uint4& q, int* v) {
+  v[0] = static_cast<int>(q.x); v[1] = static_cast<int>(q.y); v[2] = static_cast<int>(q.z); v[3] = static_cast<int>(q.w);
+}
+__device__ __forceinline__ uint4 pack16(const float* v) {
+  return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+}
+__device__ __forceinline__ uint4 pack16(const double* v) {
+  return make_uint4(static_cast<uint32_t>(__double2loint(v[0])), static_cast<uint32_t>(__double2hiint(v[0])),
+                    static_cast<uint32_t>(__double2loint(v[1])), static_cast<uint32_t>(__double2hiint(v[1])));
+}
+
 #ifdef MOEP_SILU_ACCURATE
 __device__ __forceinline__ float silu_f32(float a) { return __fdiv_rn(a, 1.0f + expf(-a)); }
 #else

@@ -63,7 +63,7 @@ __device__ __forceinline__ void top_keys(const T* myrow, uint32_t (&top)[G]) {
     for (int c = 0; c < G; c += R::V) {
       const uint4 q = *reinterpret_cast<const uint4*>(myrow + g0 + c);
       T v[R::V];
-      *reinterpret_cast<uint4*>(v) = q;
+      unpack16(q, v);
 #pragma unroll
       for (int u = 0; u < R::V; ++u) {
         const int e = g0 + c + u;
@@ -290,7 +290,7 @@ labels_rows_kernel(const T* __restrict__ sc, int64_t n, int k, int top_cut, int*
 #pragma unroll
     for (int c = 0; c < E; c += R::V) {
       T v[R::V];
-      *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(myrow + c);
+      unpack16(*reinterpret_cast<const uint4*>(myrow + c), v);
 #pragma unroll
       for (int u = 0; u < R::V; ++u) key[c + u] = (okey(v[u]) & ~63u) | static_cast<uint32_t>(63 - (c + u));
     }
