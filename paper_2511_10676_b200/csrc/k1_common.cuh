@@ -141,15 +141,16 @@ __device__ __forceinline__ void row_epilogue_core(const Params& p, ZGet zv, bool
   // in their top 26 bits; otherwise (ties, near-ties: rare) the exact
   // repeated argmax below. ~3x fewer instructions than P argmax rounds.
   bool net_ok = false;
-  if constexpr (EP >= 16 && EP <= 64) {
+  if constexpr (EP >= 16 && EP <= 128) {
     using namespace moep::sortnet;
+    constexpr int IB = EP > 64 ? 7 : 6;  // index bits of the packed key
     uint32_t top[16], grp[16];
 #pragma unroll
     for (int g0 = 0; g0 < EP; g0 += 16) {
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int e = g0 + u;
-        grp[u] = e < p.E ? ((okey(zv(e)) & ~63u) | static_cast<uint32_t>(63 - e)) : 0u;  // padding sorts last
+        grp[u] = e < p.E ? pk_make<IB>(okey(zv(e)), e) : 0u;  // padding sorts last
       }
       sort_desc<16>(grp);
       if (g0 == 0) {
@@ -160,15 +161,15 @@ __device__ __forceinline__ void row_epilogue_core(const Params& p, ZGet zv, bool
       }
     }
     // the first P positions are exact when every adjacent pair up to position P
-    // is decided in the top 26 bits (position P: the set of the first P), P < 16
+    // is decided above the index bits (position P: the set of the first P), P < 16
     bool amb = P >= 16;
 #pragma unroll
     for (int i = 1; i < 16; ++i)
-      if (i <= P) amb |= ambiguous(top[i - 1], top[i]);
-    net_ok = !amb && (top[P < 16 ? P : 15] & ~63u) != 0u;  // a NaN / padding key inside: exact path
+      if (i <= P) amb |= ambiguous_b<IB>(top[i - 1], top[i]);
+    net_ok = !amb && (top[P < 16 ? P : 15] >> IB) != 0u;  // a NaN / padding key inside: exact path
 #pragma unroll
     for (int s = 0; s < kMaxSel; ++s) {
-      const int e = pk_index(top[s < 16 ? s : 15]);
+      const int e = pk_index_b<IB>(top[s < 16 ? s : 15]);
       tv[s] = s < P ? zv(e) : -INFINITY;
       tix[s] = s < P ? e : 0;
     }

@@ -76,5 +76,18 @@ __device__ __forceinline__ bool ambiguous(uint32_t hi_side, uint32_t lo_side) {
   return ((hi_side ^ lo_side) & ~63u) == 0;
 }
 
+// the same with IB index bits (E <= 2^IB): keys (okey & ~(2^IB - 1)) | (2^IB - 1 - e)
+template <int IB>
+__device__ __forceinline__ uint32_t pk_make(uint32_t ok, int e) {
+  constexpr uint32_t M = (1u << IB) - 1u;
+  return (ok & ~M) | (M - static_cast<uint32_t>(e));
+}
+template <int IB>
+__device__ __forceinline__ int pk_index_b(uint32_t p) { return static_cast<int>(((1u << IB) - 1u) - (p & ((1u << IB) - 1u))); }
+template <int IB>
+__device__ __forceinline__ bool ambiguous_b(uint32_t hi_side, uint32_t lo_side) {
+  return ((hi_side ^ lo_side) & ~((1u << IB) - 1u)) == 0;
+}
+
 }  // namespace sortnet
 }  // namespace moep
