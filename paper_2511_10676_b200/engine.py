@@ -197,12 +197,13 @@ class DevicePredictor:
         n = x.shape[0]
         code = MOEP_F64 if x.dtype == torch.float64 else _lib.MOEP_F32
         xb = torch.empty((n, self.d), dtype=torch.bfloat16, device=self.device)
-        cst = torch.zeros(2, dtype=torch.int32, device=self.device)
+        words = torch.zeros(4, dtype=torch.int32, device=self.device)  # cast status [2], K1 status, flag count
+        cst, kst = words[0:2], words[2:3]
         check(lib().moep_input_norm(ptr(x), code, n, self.d, 0, None, None, 0.0, ptr(xb), ptr(cst),
                                     _stream(self.device)), "moep_input_norm")
         ids = torch.empty((n, m), dtype=torch.int32, device=self.device)
-        kst = self.new_status()
-        flags, flist, fcount = self._k1(xb, m_sel=m, bounds=(m,) if m < self.E else (), ids=ids, status=kst)
+        flags, flist, fcount = self._k1(xb, m_sel=m, bounds=(m,) if m < self.E else (), ids=ids, status=kst,
+                                        flag_count=words[3:4])
         a = self._fp64_args(xb, MOEP_BF16, rows=flist, row_count=fcount, m_sel=m, ids=ids)
         self._fixup(a, n)
         return ids, cst, kst
@@ -273,11 +274,12 @@ class DevicePredictor:
         return a
 
     def _k1(self, xb, m_sel=0, bounds=(), ids=None, logits=None, truth=None, k=0, m_values=(),
-            partials=None, status=None, kernel=0, probs=None):
+            partials=None, status=None, kernel=0, probs=None, flag_count=None):
         n = xb.shape[0]
         flags = torch.empty(n, dtype=torch.uint8, device=self.device)
         flag_list = torch.empty(n, dtype=torch.int32, device=self.device)
-        flag_count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        if flag_count is None:  # else: the caller's zeroed int32[1]
+            flag_count = torch.zeros(1, dtype=torch.int32, device=self.device)
         a = _lib.PredictArgs()
         a.n_tokens, a.d, a.hidden, a.n_experts, a.arch = n, self.d, self.hidden, self.E, self.arch_code
         a.x, a.w1, a.w2 = ptr(xb), ptr(self.w1_bf16), ptr(self.w2_bf16)
