@@ -96,11 +96,7 @@ __device__ __forceinline__ void tma_cg2(const CUtensorMap* m, uint64_t* bar, voi
 // leader (the peer bit of the barrier address cleared, as the 2-SM forms expect)
 __device__ __forceinline__ void tma_cg2_mc(const CUtensorMap* m, uint64_t* bar, void* dst, int32_t c0, int32_t c1,
                                            uint16_t mask, uint64_t policy) {
-#ifdef K1V5_MBAR_MAPA
-  const uint32_t lb = mapa_shared(smem_u32(bar), cluster_ctarank() & ~1u);
-#else
   const uint32_t lb = smem_u32(bar) & 0xFEFFFFFFu;
-#endif
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
       ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
