@@ -15,14 +15,12 @@ namespace sortnet {
 // monotone unsigned image of the value: larger value -> larger key; -0 == +0;
 // NaN -> 0 (below -inf)
 __device__ __forceinline__ uint32_t okey(float v) {
-  int b = __float_as_int(v);
-  if (b == static_cast<int>(0x80000000u)) b = 0;
+  const int b = __float_as_int(__fadd_rn(v, 0.0f));  // -0 + 0 = +0 (an FMA-pipe op instead of compare / select)
   const uint32_t u = static_cast<uint32_t>(b >= 0 ? (b | 0x80000000) : ~b);
   return ((b & 0x7fffffff) > 0x7f800000) ? 0u : u;
 }
 __device__ __forceinline__ uint32_t okey(double v) {
-  long long b = __double_as_longlong(v);
-  if (b == static_cast<long long>(0x8000000000000000ull)) b = 0;
+  const long long b = __double_as_longlong(__dadd_rn(v, 0.0));
   const unsigned long long u = static_cast<unsigned long long>(b >= 0 ? (b | static_cast<long long>(0x8000000000000000ull)) : ~b);
   const bool nan = (b & 0x7fffffffffffffffll) > 0x7ff0000000000000ll;
   return nan ? 0u : static_cast<uint32_t>(u >> 32);  // top 32 bits (the low 6 are replaced by the index)
