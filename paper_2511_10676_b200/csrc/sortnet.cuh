@@ -16,8 +16,8 @@ namespace sortnet {
 // NaN -> 0 (below -inf)
 __device__ __forceinline__ uint32_t okey(float v) {
   const int b = __float_as_int(__fadd_rn(v, 0.0f));  // -0 + 0 = +0 (an FMA-pipe op instead of compare / select)
-  const uint32_t u = static_cast<uint32_t>(b >= 0 ? (b | 0x80000000) : ~b);
-  return ((b & 0x7fffffff) > 0x7f800000) ? 0u : u;
+  const uint32_t u = static_cast<uint32_t>(b ^ ((b >> 31) | static_cast<int>(0x80000000u)));  // b >= 0 ? b | 2^31 : ~b
+  return v != v ? 0u : u;  // NaN lowest
 }
 __device__ __forceinline__ uint32_t okey(double v) {
   const long long b = __double_as_longlong(__dadd_rn(v, 0.0));
