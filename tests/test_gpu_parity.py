@@ -544,3 +544,37 @@ def test_fused_softmax_probs(pb, O, arch, d, h, e, n):
     bound = pref * (np.expm1(delta)[:, None] + 1e-5) + 2.0 ** -22
     assert (np.abs(p - pref) <= bound).all(), np.abs(p - pref).max()
     assert np.allclose(p.sum(axis=1), 1.0, rtol=0, atol=1e-5)
+
+
+@pytest.mark.parametrize("e,k", [(64, 6), (128, 8), (32, 4)])
+def test_network_selection_ties_and_near_ties(pb, O, e, k):
+    """K1's token selection (packed-key bitonic network) at v4 scale with
+    exact ties (duplicate W2 rows) and near-ties (W2 rows one bf16 ulp apart
+    in one element: logits equal in their top bits but distinct): those rows
+    take the exact argmax path; ids and every counter equal the oracle's."""
+    rng = np.random.default_rng(77 + e)
+    n, d, h = 40000, 1024, 1024
+    m = bf16_model(pb, O, "arch2", d, h, e, seed=13)
+    m.w2[5] = m.w2[2]
+    m.w2[9] = m.w2[2]
+    m.w2[11] = m.w2[3].copy()
+    j = int(np.argmax(np.abs(m.w2[11])))
+    # one bf16 ulp up in one element (stays bf16-exact)
+    mant, ex = np.frexp(m.w2[11, j])
+    m.w2[11, j] = np.ldexp(mant + np.sign(mant) / 256.0, ex)
+    assert np.array_equal(O.round_bf16(m.w2), m.w2)
+    x = O.round_bf16(rng.standard_normal((n, d)))
+    zref = O.predict_logits(oracle_params(m), x)
+    truth = O.top_k_batch(zref + 0.01 * rng.standard_normal(zref.shape), k)
+    ms = O.default_m_list(k, e)
+    oc = O.eval_counters(zref, truth, e, ms)
+    dev = m.to_device()
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    for mm in (1, k, k + 2):
+        assert np.array_equal(dev.topk(xt, mm).cpu().numpy(), O.top_k_batch(zref, mm)), mm
+    cnt, _, ids = dev.evaluate(xt, torch.from_numpy(truth), k, ms, ids_m=k)
+    assert np.array_equal(ids.cpu().numpy(), O.top_k_batch(zref, k))
+    c = pb.EvalCounters.from_array(cnt.cpu().numpy(), k, e, sorted(set(ms) | {k}))
+    assert c.n == oc["n"] and c.top1 == oc["top1_count"]
+    assert c.overprov == oc["overprov_count"] and c.recall == oc["recall_count"]
+    assert np.array_equal(c.per_expert_hits, oc["per_expert_hits"])
